@@ -1,0 +1,171 @@
+/*
+ * choldiff.h -- C ABI of libcholdiff.so: B200 (sm_100a) kernels that propagate
+ * derivatives through the Cholesky decomposition Sigma = L L^T
+ * (arXiv 1602.07527, "the paper"; PAPER.md line numbers below).
+ *
+ *   reverse mode  cd_chol_rev*:  (L, Lbar)      -> Sigma_bar
+ *   forward mode  cd_chol_fwd*:  (L, Sigma_dot) -> L_dot
+ *
+ * ---------------------------------------------------------------------------
+ * Layout (all entry points)
+ *   - Matrices are n x n, COLUMN-MAJOR (LAPACK): element (i, j), 0-based, of a
+ *     matrix at pointer P with leading dimension ld is P[i + j*ld]; ld >= max(1,n).
+ *   - Only the LOWER triangle (i >= j) of L, Lbar and Sigma_dot is ever read
+ *     (PAPER.md:448-451, 612-613).  The upper triangle of L may hold anything
+ *     (e.g. Sigma); it is never read.
+ *   - Element type per cd_dtype: CD_F64 = IEEE double, CD_F32 = IEEE float.
+ *   - Batched variants: either base + stride (matrix b at P + b*stride elements,
+ *     stride >= ld*n, e.g. a contiguous batch has ld = n, stride = n*n), or a
+ *     DEVICE array of DEVICE pointers (cuBLAS "...Batched" style).
+ *
+ * In-place semantics
+ *   - Reverse: on entry tril(Abar) = Lbar; on exit tril(Abar) = tril(Sigma_bar),
+ *     the paper's Eq. 10 convention: Sigma_bar_kl = df/dSigma_kl
+ *     with Sigma_kl = Sigma_lk counted as ONE variable.  out_mode selects what is
+ *     written (cd_out_mode below).
+ *   - Forward: on entry tril(Adot) = tril(Sigma_dot) (Sigma_dot symmetric, only
+ *     its lower triangle is read); on exit tril(Adot) = L_dot.
+ *   - The upper triangle of Abar / Adot is never read, and is not written in
+ *     CD_OUT_TRIL mode (the default).
+ *   - L must not overlap Abar / Adot.
+ *
+ * Ownership
+ *   - The caller owns every buffer.  All pointers are DEVICE pointers unless the
+ *     function name ends in _host.  The library never allocates device memory,
+ *     never frees, and retains no pointer past the call's enqueue.
+ *   - `ws` is a device workspace of at least cd_workspace_size(...) bytes,
+ *     256-byte aligned; it may be NULL only when that size is 0.
+ *
+ * Streams and errors
+ *   - All work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream); the host call returns after enqueue (asynchronous).
+ *   - Return value: CD_SUCCESS (0) when the work was enqueued; -i when argument
+ *     i (1-based position in the C signature) is invalid (LAPACK INFO style:
+ *     n < 0, ld < max(1,n), stride too small, bad enum, NULL pointer with work
+ *     to do, workspace too small); CD_ERR_CUDA when a launch failed
+ *     (cd_status_string / cd_last_cuda_error give the text); CD_ERR_UNSUPPORTED
+ *     for a valid but unimplemented combination.
+ *   - Numerical status is asynchronous: if `d_info` (device int[batch], may be
+ *     NULL) is given, d_info[b] = 0 when matrix b was processed normally, or
+ *     j > 0 (1-based) when L[j-1, j-1] is zero or non-finite (the first such j);
+ *     outputs of that matrix are then unspecified.  Other non-finite inputs are
+ *     not checked (finiteness is a precondition).
+ *   - n = 0 or batch = 0 is a no-op returning CD_SUCCESS.
+ *   - Reentrant; no global mutable state except a per-process cache of kernel
+ *     attributes.  L may be shared read-only by concurrent calls.
+ */
+#ifndef CHOLDIFF_H
+#define CHOLDIFF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CD_VERSION 100 /* 1.0.0 */
+
+typedef struct CUstream_st* cd_stream_t; /* == cudaStream_t */
+
+typedef enum { CD_F64 = 0, CD_F32 = 1 } cd_dtype;
+typedef enum { CD_OP_REV = 0, CD_OP_FWD = 1 } cd_op;
+
+/* Route (the symbolic result may be preferable for small
+ * matrices).  AUTO chooses by size; ALGORITHMIC = the paper's unblocked/blocked
+ * sweeps; SYMBOLIC = Eq. 10 / Eq. 8 (reverse: small-N
+ * batched kernel only, n <= 32). */
+typedef enum { CD_ROUTE_AUTO = 0, CD_ROUTE_ALGORITHMIC = 1, CD_ROUTE_SYMBOLIC = 2 } cd_route;
+
+/* Reverse-mode output convention (reading c1):
+ *   TRIL: tril(Sigma_bar) of Eq. 10, lower triangle only (default);
+ *   SYM : the full symmetric Sigma_bar = S + S^T - diag(S) of Eq. 9:
+ *         lower as TRIL, upper triangle written as its exact mirror;
+ *   GRAD: G = (S + S^T)/2, the symmetric-gradient convention of autograd
+ *         frameworks: off-diagonal entries of Eq. 9 halved, both triangles written.
+ * Forward mode accepts TRIL only. */
+typedef enum { CD_OUT_TRIL = 0, CD_OUT_SYM = 1, CD_OUT_GRAD = 2 } cd_out_mode;
+
+typedef struct cd_opts {
+  int32_t nb;       /* block size N_b of the blocked sweeps; 0 = auto */
+  int32_t route;    /* cd_route   */
+  int32_t out_mode; /* cd_out_mode */
+  int32_t flags;    /* reserved, must be 0 */
+} cd_opts;          /* NULL opts = {0, CD_ROUTE_AUTO, CD_OUT_TRIL, 0} */
+
+enum {
+  CD_SUCCESS = 0,
+  CD_ERR_CUDA = 1,        /* a CUDA launch / copy failed */
+  CD_ERR_UNSUPPORTED = 2  /* valid arguments, combination not implemented */
+};
+
+/* Single matrix, reverse mode: tril(Abar) = Lbar -> tril(Sigma_bar) (in place).
+ * Blocked sweep of PAPER.md:689-701 for n > the on-chip limit, unblocked on-chip
+ * sweep otherwise. */
+int cd_chol_rev(cd_dtype dt, int64_t n, const void* L, int64_t ldl, void* Abar, int64_t ldabar,
+                const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream);
+
+/* Single matrix, forward mode: tril(Adot) = tril(Sigma_dot) -> L_dot (in place).
+ * PAPER.md:655-666 (blocked) / 489-498 (unblocked). */
+int cd_chol_fwd(cd_dtype dt, int64_t n, const void* L, int64_t ldl, void* Adot, int64_t ldadot,
+                const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream);
+
+/* Batched, base + stride (strides in ELEMENTS). */
+int cd_chol_rev_strided_batched(cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t strideL,
+                                void* Abar, int64_t ldabar, int64_t strideAbar, int64_t batch,
+                                const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
+                                cd_stream_t stream);
+int cd_chol_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t strideL,
+                                void* Adot, int64_t ldadot, int64_t strideAdot, int64_t batch,
+                                const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
+                                cd_stream_t stream);
+
+/* Batched, device arrays of device pointers (L_array[b], Abar_array[b]). */
+int cd_chol_rev_batched(cd_dtype dt, int64_t n, const void* const* L_array, int64_t ldl,
+                        void* const* Abar_array, int64_t ldabar, int64_t batch, const cd_opts* opts,
+                        void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream);
+int cd_chol_fwd_batched(cd_dtype dt, int64_t n, const void* const* L_array, int64_t ldl,
+                        void* const* Adot_array, int64_t ldadot, int64_t batch, const cd_opts* opts,
+                        void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream);
+
+/* Device workspace (bytes) that a call with these arguments needs; 0 if none.
+ * `batch` = 1 for the single-matrix calls.  For the pointer-array batched calls
+ * pass the batch size as well. */
+size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts);
+
+/* Host-buffer convenience for one matrix (end-to-end measurement path): copies
+ * the dense n x n column-major host arrays L and A (ld = n) to the device
+ * workspace, runs cd_chol_rev / cd_chol_fwd there, and copies A back.
+ * `ws` must hold cd_workspace_size_host(...) bytes.  Host buffers should be
+ * pinned for the copies to be asynchronous; the call is asynchronous on `stream`
+ * (synchronize before reading A). */
+size_t cd_workspace_size_host(cd_op op, cd_dtype dt, int64_t n, const cd_opts* opts);
+int cd_chol_host(cd_op op, cd_dtype dt, int64_t n, const void* L_host, void* A_host,
+                 const cd_opts* opts, void* ws, size_t ws_bytes, cd_stream_t stream);
+
+const char* cd_status_string(int status);
+const char* cd_last_cuda_error(void); /* text of the last CUDA error seen by this thread */
+int cd_version(void);
+
+/* Number of kernel launches the library enqueued on this thread since the last
+ * reset (evidence for bench.py's "gpu_launches"). */
+int64_t cd_launch_count(void);
+void cd_reset_launch_count(void);
+
+/* Kernel-class timing (measurement evidence for bench.py's roofline).  While
+ * enabled, the library brackets every launch it enqueues on this thread with a
+ * pair of CUDA events on the launch stream and records the launch's ALGORITHMIC
+ * flop count (the paper's operation count for that update, e.g. 2*M*N*K for
+ * Bbar -= Cbar R, p*w*(w+1) for the panel solve Cbar D^{-1}).  cd_profile_read
+ * synchronizes the recorded events and returns, for kernel class `cls`
+ * (CD_PROF_GEMM, CD_PROF_REDUCE, CD_PROF_SWEEP, CD_PROF_TRINV, CD_PROF_OTHER),
+ * the summed device time (ms), flops and launch count.  Returns 0 or CD_ERR_CUDA. */
+enum { CD_PROF_GEMM = 0, CD_PROF_REDUCE = 1, CD_PROF_SWEEP = 2, CD_PROF_TRINV = 3, CD_PROF_OTHER = 4, CD_PROF_NCLS = 5 };
+void cd_profile_enable(int on);
+void cd_profile_reset(void);
+int cd_profile_read(int cls, double* ms, double* flops, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHOLDIFF_H */

@@ -1,0 +1,240 @@
+"""paper_1602_07527_b200 -- thin Python binding of libcholdiff.so (include/choldiff.h).
+
+Derivatives of the Cholesky decomposition Sigma = L L^T on B200 (arXiv 1602.07527):
+
+* ``chol_rev(L, Lbar)``  -> tril(Sigma_bar)  (reverse mode)
+* ``chol_fwd(L, Sdot)``  -> L_dot            (forward mode)
+
+Arguments are torch CUDA tensors (float64 or float32) holding one (N, N) matrix or
+a batch (B, N, N), in *logical* orientation with COLUMN-MAJOR memory per matrix,
+i.e. ``t.stride(-2) == 1`` (``colmajor(t)`` makes such a copy).  Only lower
+triangles are read.  The computation is in place on the second argument (as in
+the paper) unless ``inplace=False``.
+
+This module only marshals arguments (pointers, leading dimensions, the current
+torch stream and a workspace tensor) into the C ABI; every arithmetic step runs in
+the CUDA kernels of the library.  There is no CPU fallback: if the library is
+missing or no GPU is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from . import _build
+
+__all__ = ["chol_rev", "chol_fwd", "chol_host", "colmajor", "workspace_size", "lib", "library_path",
+           "launch_count", "reset_launch_count", "CholdiffError", "OUT_MODES", "ROUTES"]
+
+CD_F64, CD_F32 = 0, 1
+CD_OP_REV, CD_OP_FWD = 0, 1
+ROUTES = {"auto": 0, "algorithmic": 1, "symbolic": 2}
+OUT_MODES = {"tril": 0, "sym": 1, "grad": 2}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class CholdiffError(RuntimeError):
+    pass
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("nb", ctypes.c_int32), ("route", ctypes.c_int32), ("out_mode", ctypes.c_int32),
+                ("flags", ctypes.c_int32)]
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    """Load libcholdiff.so (building it first if the sources are newer)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _build.LIB
+            if not os.path.exists(path) or _build.stale():
+                _build.build()
+            L = ctypes.CDLL(path)
+            vp, i64, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t
+            po = ctypes.POINTER(_Opts)
+            for name in ("cd_chol_rev", "cd_chol_fwd"):
+                f = getattr(L, name)
+                f.argtypes = [ctypes.c_int, i64, vp, i64, vp, i64, po, vp, sz, vp, vp]
+                f.restype = ctypes.c_int
+            for name in ("cd_chol_rev_strided_batched", "cd_chol_fwd_strided_batched"):
+                f = getattr(L, name)
+                f.argtypes = [ctypes.c_int, i64, vp, i64, i64, vp, i64, i64, i64, po, vp, sz, vp, vp]
+                f.restype = ctypes.c_int
+            for name in ("cd_chol_rev_batched", "cd_chol_fwd_batched"):
+                f = getattr(L, name)
+                f.argtypes = [ctypes.c_int, i64, vp, i64, vp, i64, i64, po, vp, sz, vp, vp]
+                f.restype = ctypes.c_int
+            L.cd_workspace_size.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, po]
+            L.cd_workspace_size.restype = sz
+            L.cd_workspace_size_host.argtypes = [ctypes.c_int, ctypes.c_int, i64, po]
+            L.cd_workspace_size_host.restype = sz
+            L.cd_chol_host.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, po, vp, sz, vp]
+            L.cd_chol_host.restype = ctypes.c_int
+            L.cd_status_string.argtypes = [ctypes.c_int]
+            L.cd_status_string.restype = ctypes.c_char_p
+            L.cd_last_cuda_error.restype = ctypes.c_char_p
+            L.cd_version.restype = ctypes.c_int
+            L.cd_launch_count.restype = i64
+            L.cd_reset_launch_count.restype = None
+            _lib = L
+    return _lib
+
+
+def launch_count() -> int:
+    return int(lib().cd_launch_count())
+
+
+def reset_launch_count() -> None:
+    lib().cd_reset_launch_count()
+
+
+def _check(rc: int):
+    if rc != 0:
+        L = lib()
+        msg = L.cd_status_string(rc).decode()
+        if rc == 1:
+            msg += ": " + L.cd_last_cuda_error().decode()
+        raise CholdiffError(f"libcholdiff status {rc}: {msg}")
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return CD_F64
+    if t.dtype == torch.float32:
+        return CD_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (float64 / float32 only)")
+
+
+def colmajor(t: torch.Tensor) -> torch.Tensor:
+    """Copy of a logical (..., N, N) tensor whose per-matrix memory is column-major."""
+    return t.transpose(-1, -2).contiguous().transpose(-1, -2)
+
+
+def is_colmajor(t: torch.Tensor) -> bool:
+    n = t.shape[-1]
+    if t.shape[-2] != n:
+        return False
+    if n <= 1:
+        return True
+    ok = t.stride(-2) == 1 and t.stride(-1) >= n
+    if t.dim() == 3 and t.shape[0] > 1:
+        ok = ok and t.stride(0) >= t.stride(-1) * n
+    return ok
+
+
+def _opts(nb, route, out):
+    return _Opts(int(nb or 0), ROUTES[route], OUT_MODES[out], 0)
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device: torch.device) -> torch.Tensor | None:
+    if nbytes == 0:
+        return None
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def workspace_size(op: str, dtype: torch.dtype, n: int, batch: int = 1, nb=None, route="auto", out="tril") -> int:
+    o = _opts(nb, route, out)
+    return int(lib().cd_workspace_size(CD_OP_REV if op == "rev" else CD_OP_FWD,
+                                       CD_F64 if dtype == torch.float64 else CD_F32, n, batch, ctypes.byref(o)))
+
+
+def _prep(L: torch.Tensor, A: torch.Tensor, inplace: bool):
+    if not (L.is_cuda and A.is_cuda):
+        raise CholdiffError("chol_rev/chol_fwd take CUDA tensors (use chol_host for host buffers)")
+    if L.dtype != A.dtype:
+        raise TypeError("L and the sensitivity must have the same dtype")
+    if L.shape != A.shape or L.dim() not in (2, 3) or L.shape[-1] != L.shape[-2]:
+        raise ValueError(f"expected matching (N,N) or (B,N,N) tensors, got {tuple(L.shape)} / {tuple(A.shape)}")
+    if not is_colmajor(L):
+        L = colmajor(L)
+    if not inplace or not is_colmajor(A):
+        A = colmajor(A)
+    return L, A
+
+
+def _run(op: int, L: torch.Tensor, A: torch.Tensor, nb, route, out, info: bool):
+    Lc = lib()
+    n = A.shape[-1]
+    batch = A.shape[0] if A.dim() == 3 else 1
+    if n == 0 or batch == 0:  # no-op (the C ABI returns CD_SUCCESS as well)
+        return (A, torch.zeros(batch, dtype=torch.int32, device=A.device)) if info else A
+    o = _opts(nb, route, out)
+    dt = _dt(A)
+    dev = A.device
+    with torch.cuda.device(dev):
+        nbytes = int(Lc.cd_workspace_size(op, dt, n, batch, ctypes.byref(o)))
+        ws = _workspace(nbytes, dev)
+        info_t = torch.zeros(batch, dtype=torch.int32, device=dev) if info else None
+        stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        ldl = max(1, L.stride(-1)) if n > 1 else max(1, n)
+        lda = max(1, A.stride(-1)) if n > 1 else max(1, n)
+        wsp = ctypes.c_void_p(ws.data_ptr()) if ws is not None else None
+        ip = ctypes.c_void_p(info_t.data_ptr()) if info_t is not None else None
+        if A.dim() == 2:
+            f = Lc.cd_chol_rev if op == CD_OP_REV else Lc.cd_chol_fwd
+            rc = f(dt, n, L.data_ptr(), ldl, A.data_ptr(), lda, ctypes.byref(o), wsp, nbytes, ip, stream)
+        else:
+            f = Lc.cd_chol_rev_strided_batched if op == CD_OP_REV else Lc.cd_chol_fwd_strided_batched
+            sL = L.stride(0) if batch > 1 else ldl * n
+            sA = A.stride(0) if batch > 1 else lda * n
+            rc = f(dt, n, L.data_ptr(), ldl, sL, A.data_ptr(), lda, sA, batch, ctypes.byref(o), wsp, nbytes, ip,
+                   stream)
+        _check(rc)
+    return (A, info_t) if info else A
+
+
+def chol_rev(L: torch.Tensor, Lbar: torch.Tensor, *, nb=None, route: str = "auto", out: str = "tril",
+             inplace: bool = True, info: bool = False):
+    """Reverse mode (L, Lbar) -> Sigma_bar.  Returns the tensor holding tril(Sigma_bar)
+    (Eq. 10 convention; ``out='sym'`` / ``'grad'`` also write the upper triangle, see
+    include/choldiff.h).  With ``info=True`` also returns the per-matrix status tensor."""
+    L, A = _prep(L, Lbar, inplace)
+    return _run(CD_OP_REV, L, A, nb, route, out, info)
+
+
+def chol_fwd(L: torch.Tensor, Sdot: torch.Tensor, *, nb=None, route: str = "auto", inplace: bool = True,
+             info: bool = False):
+    """Forward mode (L, Sigma_dot) -> L_dot (lower triangle of the returned tensor)."""
+    L, A = _prep(L, Sdot, inplace)
+    return _run(CD_OP_FWD, L, A, nb, route, "tril", info)
+
+
+def chol_host(op: str, L_host: torch.Tensor, A_host: torch.Tensor, *, nb=None, device=None) -> torch.Tensor:
+    """End-to-end path with HOST buffers (cd_chol_host): dense column-major host arrays
+    (pinned for asynchronous copies) are copied to the device, processed and copied
+    back into ``A_host`` in place.  Synchronizes the current stream before returning."""
+    Lc = lib()
+    dev = torch.device(device or "cuda")
+    n = A_host.shape[-1]
+    dt = _dt(A_host)
+    o = _opts(nb, "auto", "tril")
+    opc = CD_OP_REV if op == "rev" else CD_OP_FWD
+    if not (L_host.stride(-2) == 1 and L_host.stride(-1) == n and A_host.stride(-2) == 1 and A_host.stride(-1) == n):
+        raise ValueError("chol_host expects dense column-major (ld = N) host tensors")
+    with torch.cuda.device(dev):
+        nbytes = int(Lc.cd_workspace_size_host(opc, dt, n, ctypes.byref(o)))
+        ws = _workspace(nbytes, dev)
+        stream = torch.cuda.current_stream(dev)
+        rc = Lc.cd_chol_host(opc, dt, n, L_host.data_ptr(), A_host.data_ptr(), ctypes.byref(o),
+                             ctypes.c_void_p(ws.data_ptr()), nbytes, ctypes.c_void_p(stream.cuda_stream))
+        _check(rc)
+        stream.synchronize()
+    return A_host

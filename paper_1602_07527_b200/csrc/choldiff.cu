@@ -1,0 +1,640 @@
+// choldiff.cu -- C ABI (include/choldiff.h) and host drivers of libcholdiff.so.
+//
+// Dispatch (per call):
+//   n <= 32          one warp per matrix            (sweep_warp.cuh)   PAPER.md:566-578 / 489-498
+//   n <= CTA_NMAX    one CTA per matrix             (sweep_cta.cuh)
+//   larger n         blocked sweep (PAPER.md:689-701 reverse, 655-666 forward):
+//                    diagonal-block inverses (k_trinv) once per call, then per block
+//                    step the Level-3 updates as DMMA GEMMs (gemm.cuh) around the
+//                    shared-memory diagonal-block kernel.
+// All launches go to the caller's stream; the driver never synchronizes.
+//
+// Workspace: every driver runs in two modes, "plan" (no launches, only workspace
+// carving) and "run"; cd_workspace_size returns the plan's high-water mark, so the
+// size query and the launch sequence can never disagree.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/choldiff.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "misc.cuh"
+#include "sweep_cta.cuh"
+#include "sweep_warp.cuh"
+
+namespace cd {
+
+static thread_local int64_t g_launches = 0;
+static thread_local char g_cuda_err[256] = "";
+
+// ---- optional per-launch timing (cd_profile_*) ----
+struct ProfRec {
+  cudaEvent_t a, b;
+  int cls;
+  double flops;
+};
+struct Prof {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+static thread_local Prof g_prof;
+
+static int note_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return CD_SUCCESS;
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return CD_ERR_CUDA;
+}
+
+struct Ctx {
+  bool plan;            // plan mode: carve workspace only
+  char* ws;             // device workspace base (run mode)
+  size_t off = 0;       // high-water mark
+  cudaStream_t st;
+  int sms = 148;
+  int err = CD_SUCCESS;
+  void* take(size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    void* p = plan ? nullptr : ws + off;
+    off += bytes;
+    return p;
+  }
+  bool ok() const { return err == CD_SUCCESS; }
+  // call before a launch: opens a timing bracket when profiling is on
+  void pre(int cls, double flops) {
+    if (!g_prof.on) return;
+    ProfRec r{g_prof.ev(), g_prof.ev(), cls, flops};
+    cudaEventRecord(r.a, st);
+    g_prof.recs.push_back(r);
+  }
+  void launched() {
+    ++g_launches;
+    if (g_prof.on && !g_prof.recs.empty()) cudaEventRecord(g_prof.recs.back().b, st);
+    if (err == CD_SUCCESS) err = note_cuda(cudaGetLastError());
+  }
+};
+
+static int grid_1d(int64_t total, int threads, int sms) {
+  int64_t g = (total + threads - 1) / threads;
+  return int(std::max<int64_t>(1, std::min<int64_t>(g, int64_t(sms) * 16)));
+}
+
+// ------------------------------------------------------------------ kernel attribute setup
+template <typename K>
+static void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+// ------------------------------------------------------------------ GEMM launcher
+constexpr int64_t PART_TILES = 2 * 152;  // split-K partial budget, in 128x128 output tiles
+
+template <typename T>
+struct Gemm {
+  Ctx& c;
+  GemmParams p{};
+  int TA = 0, TB = 0;
+  double algo_flops = -1.0;  // the paper's flop count for this update (default 2*M*N*sum K)
+  explicit Gemm(Ctx& ctx, int M, int N, int ta, int tb, int64_t batch) : c(ctx), TA(ta), TB(tb) {
+    p.M = M;
+    p.N = N;
+    p.batch = batch;
+    p.nseg = 0;
+    p.alpha = 1.0;
+    p.beta = 0.0;
+  }
+  Gemm& seg(Opnd A, Opnd B, int K) {
+    if (K <= 0) return *this;
+    constexpr int BK = GBK<T>::v;
+    int kv0 = 0;
+    if (p.nseg > 0) {
+      const GemmSeg& s = p.seg[p.nseg - 1];
+      kv0 = s.kv0 + ((s.K + BK - 1) / BK) * BK;
+    }
+    p.seg[p.nseg++] = GemmSeg{A, B, K, kv0};
+    return *this;
+  }
+  Gemm& flops(double f) {
+    algo_flops = f;
+    return *this;
+  }
+  // D = alpha * sum + beta * Cin
+  void run(Opnd Cin, Opnd D, double alpha, double beta, bool tril, T* part_ws) {
+    if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
+    if (p.nseg == 0) {  // nothing to accumulate: D = beta * Cin
+      if (beta == 1.0 && Cin.base == D.base && Cin.arr == D.arr && Cin.off == D.off) return;
+      // (not needed by the drivers)
+      return;
+    }
+    constexpr int BK = GBK<T>::v;
+    const GemmSeg& last = p.seg[p.nseg - 1];
+    p.KT = (last.kv0 + last.K + BK - 1) / BK;
+    p.Cin = Cin;
+    p.D = D;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.tril = tril ? 1 : 0;
+    const int64_t tiles = int64_t((p.M + G_BM - 1) / G_BM) * ((p.N + G_BN - 1) / G_BN) * p.batch;
+    int splits = 1;
+    if (tiles < c.sms && p.KT >= 4) {
+      splits = int(std::min<int64_t>((2 * c.sms + tiles - 1) / tiles, p.KT / 2));
+      const int64_t cap = PART_TILES * G_BM * G_BN / (int64_t(p.M) * p.N * p.batch);
+      splits = int(std::max<int64_t>(1, std::min<int64_t>(splits, cap)));
+    }
+    p.kt_per_split = (p.KT + splits - 1) / splits;
+    splits = (p.KT + p.kt_per_split - 1) / p.kt_per_split;
+    p.splits = splits;
+    p.part = part_ws;
+    if (c.plan || !c.ok()) return;
+    dim3 grid((p.M + G_BM - 1) / G_BM, (p.N + G_BN - 1) / G_BN, unsigned(p.batch * splits));
+    if (algo_flops < 0) {
+      int64_t ks = 0;
+      for (int s = 0; s < p.nseg; ++s) ks += p.seg[s].K;
+      algo_flops = 2.0 * p.M * double(p.N) * double(ks);
+    }
+    c.pre(CD_PROF_GEMM, algo_flops * double(p.batch));
+    launch(grid);
+    if (splits > 1) {
+      const int64_t total = int64_t(p.M) * p.N * p.batch;
+      c.pre(CD_PROF_REDUCE, 0.0);
+      k_splitk_reduce<T><<<grid_1d(total, 256, c.sms), 256, 0, c.st>>>(p.M, p.N, p.batch, splits,
+                                                                          reinterpret_cast<const T*>(part_ws), Cin,
+                                                                          D, alpha, beta, p.tril);
+      c.launched();
+    }
+  }
+  template <int A_, int B_>
+  void launch_t(dim3 grid) {
+    auto kern = k_gemm<T, A_, B_>;
+    set_smem(kern, GemmLayout<T, A_, B_>::SMEM);
+    if (p.splits > 1) {
+      // the kernel writes partials; alpha/beta/Cin are applied by the reduction
+    }
+    kern<<<grid, G_THREADS, GemmLayout<T, A_, B_>::SMEM, c.st>>>(p);
+    c.launched();
+  }
+  void launch(dim3 grid) {
+    if (TA == 0 && TB == 0) launch_t<0, 0>(grid);
+    else if (TA == 0 && TB == 1) launch_t<0, 1>(grid);
+    else if (TA == 1 && TB == 0) launch_t<1, 0>(grid);
+    else launch_t<1, 1>(grid);
+  }
+};
+
+static Opnd null_opnd() { return Opnd{nullptr, nullptr, 0, 0, 0}; }
+// sub-view of an operand: rows/cols offset
+static Opnd sub(const Opnd& o, int64_t r0, int64_t c0) {
+  Opnd s = o;
+  s.off = o.off + r0 + c0 * o.ld;
+  return s;
+}
+// dense strided workspace operand: matrix b at base + b*stride, ld
+static Opnd ws_opnd(void* base, int64_t stride, int64_t ld) { return Opnd{base, nullptr, stride, ld, 0}; }
+
+// ------------------------------------------------------------------ small-n kernels
+template <typename T>
+static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd A, int out_mode, Opnd S,
+                            int* info) {
+  if (c.plan || !c.ok()) return;
+  const double nf = n;
+  c.pre(CD_PROF_SWEEP, double(batch) * (rev ? (4 * nf * nf * nf + 3 * nf * nf + 11 * nf) / 6
+                                            : (4 * nf * nf * nf + 3 * nf * nf + 5 * nf) / 6));
+  if (n <= 32) {
+    const size_t smem = sweep_warp_smem<T>();
+    const unsigned grid = unsigned((batch + SW_WPB - 1) / SW_WPB);
+    if (rev) {
+      set_smem(k_sweep_warp_rev<T>, smem);
+      k_sweep_warp_rev<T><<<grid, SW_WPB * 32, smem, c.st>>>(n, batch, L, A, out_mode, info);
+    } else {
+      set_smem(k_sweep_warp_fwd<T>, smem);
+      k_sweep_warp_fwd<T><<<grid, SW_WPB * 32, smem, c.st>>>(n, batch, L, A, info);
+    }
+    c.launched();
+    if (S.base || S.arr) {  // (blocked driver with a tiny block) S = Dbar + Dbar^T
+      const int64_t total = int64_t(n) * n * batch;
+      c.pre(CD_PROF_OTHER, 0.0);
+      k_sym2<T><<<grid_1d(total, 256, c.sms), 256, 0, c.st>>>(n, batch, A, S, rev ? 0 : 1);
+      c.launched();
+    }
+  } else {
+    const size_t smem = sweep_cta_smem<T>(n);
+    if (rev) {
+      set_smem(k_sweep_cta_rev<T>, smem);
+      k_sweep_cta_rev<T><<<unsigned(batch), CTA_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+    } else {
+      set_smem(k_sweep_cta_fwd<T>, smem);
+      k_sweep_cta_fwd<T><<<unsigned(batch), CTA_THREADS, smem, c.st>>>(n, L, A, S, info);
+    }
+    c.launched();
+  }
+}
+
+template <typename T>
+static void run_trinv(Ctx& c, int n, int nb, bool reverse, int64_t batch, Opnd L, T* Dinv) {
+  if (c.plan || !c.ok()) return;
+  const int nblk = nblocks(n, nb);
+  const size_t smem = size_t(nb) * (nb + 1) / 2 * sizeof(T);
+  set_smem(k_trinv<T>, smem);
+  c.pre(CD_PROF_TRINV, 0.0);
+  k_trinv<T><<<dim3(nblk, unsigned(batch)), TRINV_THREADS, smem, c.st>>>(n, nb, reverse ? 1 : 0, L, Dinv, nb,
+                                                                        int64_t(nb) * nb);
+  c.launched();
+}
+
+template <typename T>
+static void run_copy(Ctx& c, int M, int N, int64_t batch, Opnd S, Opnd D) {
+  if (c.plan || !c.ok() || M <= 0 || N <= 0) return;
+  c.pre(CD_PROF_OTHER, 0.0);
+  k_copy<T><<<grid_1d(int64_t(M) * N * batch, 256, c.sms), 256, 0, c.st>>>(M, N, batch, S, D);
+  c.launched();
+}
+
+template <typename T>
+static void run_sym2(Ctx& c, int n, int64_t batch, Opnd A, Opnd S, int clean) {
+  if (c.plan || !c.ok()) return;
+  c.pre(CD_PROF_OTHER, 0.0);
+  k_sym2<T><<<grid_1d(int64_t(n) * n * batch, 256, c.sms), 256, 0, c.st>>>(n, batch, A, S, clean);
+  c.launched();
+}
+
+// ------------------------------------------------------------------ blocked reverse
+// chol_blocked_rev, block [j, k) (0-based), w = k - j, p = n - k, q = j:
+//   Cbar <- Cbar D^{-1}                      W = Abar[k:n, j:k] Dinv        (GEMM, K = w)
+//   Bbar <- Bbar - Cbar R                    Abar[k:n, 0:j] -= W L[j:k, 0:j]
+//   Dbar <- Dbar - tril(Cbar^T C)            Abar[j:k, j:k] -= tril(W^T L[k:n, j:k])  (split-K)
+//   Dbar <- chol_unblocked_rev(D, Dbar)      sweep kernel; also S = Dbar + Dbar^T
+//   Rbar <- Rbar - Cbar^T B - (Dbar+Dbar^T) R   Abar[j:k, 0:j] -= [S; W]^T L[j:n, 0:j]  (one GEMM, 2 K-segments)
+// W is written straight into Abar's Cbar region when one 128-wide N-tile covers
+// the block (each CTA then reads its rows completely before writing them);
+// otherwise through workspace + copy.
+template <typename T>
+static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, T* part_ws) {
+  const int nblk = nblocks(n, nb);
+  T* Dinv = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nblk * nb * nb));
+  T* Sws = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nb * nb));
+  const bool w_inplace = nb <= G_BN;
+  T* Wws = w_inplace ? nullptr : static_cast<T*>(c.take(sizeof(T) * size_t(batch) * n * nb));
+  run_trinv<T>(c, n, nb, true, batch, L, Dinv);
+  for (int qb = nblk - 1; qb >= 0; --qb) {
+    int j, w;
+    block_range(n, nb, true, qb, j, w);
+    const int k = j + w, p = n - k, q = j;
+    const Opnd Dinv_q = ws_opnd(Dinv + int64_t(qb) * nb * nb, int64_t(nblk) * nb * nb, nb);
+    const Opnd S = ws_opnd(Sws, int64_t(nb) * nb, w);
+    const Opnd Cbar = sub(A, k, j);
+    const Opnd W = w_inplace ? Cbar : ws_opnd(Wws, int64_t(n) * nb, std::max(p, 1));
+    if (p > 0) {
+      // Cbar <- Cbar D^{-1}
+      Gemm<T>(c, p, w, 0, 0, batch)
+          .seg(Cbar, Dinv_q, w)
+          .flops(double(p) * w * (w + 1))  // TRSM  Cbar D^{-1}
+          .run(null_opnd(), W, 1.0, 0.0, false, part_ws);
+      if (!w_inplace) run_copy<T>(c, p, w, batch, W, Cbar);
+      // Bbar <- Bbar - Cbar R
+      if (q > 0)
+        Gemm<T>(c, p, q, 0, 0, batch).seg(W, sub(L, j, 0), w).run(sub(A, k, 0), sub(A, k, 0), -1.0, 1.0, false,
+                                                                 part_ws);
+      // Dbar <- Dbar - tril(Cbar^T C)
+      Gemm<T>(c, w, w, 1, 0, batch)
+          .seg(W, sub(L, k, j), p)
+          .flops(double(w) * (w + 1) * p)  // lower triangle only
+          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, true, part_ws);
+    }
+    // Dbar <- chol_unblocked_rev(D, Dbar)  (+ S = Dbar + Dbar^T)      (w <= CTA_NMAX)
+    run_sweep_small<T>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, q > 0 ? S : null_opnd(), nullptr);
+    // Rbar <- Rbar - Cbar^T B - (Dbar + Dbar^T) R
+    if (q > 0) {
+      Gemm<T> g(c, w, q, 1, 0, batch);
+      g.seg(S, sub(L, j, 0), w);
+      if (p > 0) g.seg(W, sub(L, k, 0), p);
+      g.run(sub(A, j, 0), sub(A, j, 0), -1.0, 1.0, false, part_ws);
+    }
+  }
+  if (info && !c.plan && c.ok()) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_diag_info<T><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
+    c.launched();
+  }
+}
+
+// ------------------------------------------------------------------ blocked forward
+// chol_blocked_fwd, block [j, k), w = k - j, p = n - k, q = j:
+//   Ddot <- Ddot - tril(Rdot R^T + R Rdot^T)        GEMM (2 K-segments), tril, split-K
+//   Ddot <- chol_unblocked_fwd(D, Ddot)             sweep kernel (+ clean tril(Ddot) copy Dc)
+//   Cdot <- Cdot - Bdot R^T - B Rdot^T              } one GEMM with 3 K-segments into W:
+//   Cdot <- (Cdot - C Ddot^T) D^{-T}                }   W = Cdot - [Bdot B C][R Rdot Dc]^T
+//                                                       then Cdot = W Dinv^T
+// (W is Cdot itself when one N-tile covers the block, as in blocked_rev.)
+template <typename T>
+static void blocked_fwd(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, T* part_ws) {
+  const int nblk = nblocks(n, nb);
+  T* Dinv = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nblk * nb * nb));
+  T* Dcw = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nb * nb));
+  const bool w_inplace = nb <= G_BN;  // see blocked_rev
+  T* Wws = w_inplace ? nullptr : static_cast<T*>(c.take(sizeof(T) * size_t(batch) * n * nb));
+  run_trinv<T>(c, n, nb, false, batch, L, Dinv);
+  for (int qb = 0; qb < nblk; ++qb) {
+    int j, w;
+    block_range(n, nb, false, qb, j, w);
+    const int k = j + w, p = n - k, q = j;
+    const Opnd Dinv_q = ws_opnd(Dinv + int64_t(qb) * nb * nb, int64_t(nblk) * nb * nb, nb);
+    const Opnd Dc = ws_opnd(Dcw, int64_t(nb) * nb, w);
+    const Opnd W = w_inplace ? sub(A, k, j) : ws_opnd(Wws, int64_t(n) * nb, std::max(p, 1));
+    if (q > 0)  // Ddot <- Ddot - tril(Rdot R^T + R Rdot^T)
+      Gemm<T>(c, w, w, 0, 1, batch)
+          .seg(sub(A, j, 0), sub(L, j, 0), q)
+          .seg(sub(L, j, 0), sub(A, j, 0), q)
+          .flops(2.0 * w * (w + 1) * q)  // lower triangle only
+          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, true, part_ws);
+    run_sweep_small<T>(c, false, w, batch, sub(L, j, j), sub(A, j, j), 0, p > 0 ? Dc : null_opnd(), nullptr);
+    if (p > 0) {
+      Gemm<T> g(c, p, w, 0, 1, batch);
+      if (q > 0) g.seg(sub(A, k, 0), sub(L, j, 0), q).seg(sub(L, k, 0), sub(A, j, 0), q);
+      g.seg(sub(L, k, j), Dc, w);
+      g.run(sub(A, k, j), W, -1.0, 1.0, false, part_ws);
+      Gemm<T>(c, p, w, 0, 1, batch)
+          .seg(W, Dinv_q, w)
+          .flops(double(p) * w * (w + 1))  // TRSM  X D^{-T}
+          .run(null_opnd(), sub(A, k, j), 1.0, 0.0, false, part_ws);
+    }
+  }
+  if (info && !c.plan && c.ok()) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_diag_info<T><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
+    c.launched();
+  }
+}
+
+// ------------------------------------------------------------------ top-level
+struct Call {
+  cd_op op;
+  cd_dtype dt;
+  int64_t n, batch;
+  Opnd L, A;
+  cd_opts o;
+  int* info;
+};
+
+static int default_nb(cd_dtype dt, int64_t n) {
+  (void)dt;
+  (void)n;
+  return 128;
+}
+
+template <typename T>
+static void drive(Ctx& c, const Call& k) {
+  const int n = int(k.n);
+  if (n == 0 || k.batch == 0) return;
+  if (n <= CTA_NMAX) {
+    run_sweep_small<T>(c, k.op == CD_OP_REV, n, k.batch, k.L, k.A, k.o.out_mode, null_opnd(), k.info);
+    return;
+  }
+  const int nb = std::min(n, k.o.nb > 0 ? k.o.nb : default_nb(k.dt, n));
+  if (nb > CTA_NMAX) {  // diagonal blocks must fit the on-chip sweep / inverse kernels
+    c.err = CD_ERR_UNSUPPORTED;
+    return;
+  }
+  T* part = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
+  if (k.op == CD_OP_REV) blocked_rev<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+  else blocked_fwd<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+  if (k.op == CD_OP_REV && k.o.out_mode != CD_OUT_TRIL && !c.plan && c.ok()) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_out_mode<T><<<grid_1d(int64_t(n) * n * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, k.A, k.o.out_mode);
+    c.launched();
+  }
+}
+
+static int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      cached = v;
+    else
+      cached = 148;
+  }
+  return cached;
+}
+
+static size_t plan_size(const Call& k) {
+  Ctx c;
+  c.plan = true;
+  c.ws = nullptr;
+  c.st = nullptr;
+  if (k.dt == CD_F64) drive<double>(c, k);
+  else drive<float>(c, k);
+  return c.off;
+}
+
+static int execute(const Call& k, void* ws, size_t ws_bytes, cudaStream_t st, int ws_arg) {
+  const size_t need = plan_size(k);
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) return -ws_arg;
+  Ctx c;
+  c.plan = false;
+  c.ws = static_cast<char*>(ws);
+  c.st = st;
+  c.sms = sm_count();
+  if (k.dt == CD_F64) drive<double>(c, k);
+  else drive<float>(c, k);
+  return c.err;
+}
+
+}  // namespace cd
+
+using namespace cd;
+
+// ------------------------------------------------------------------ argument validation
+static const cd_opts kDefaultOpts = {0, CD_ROUTE_AUTO, CD_OUT_TRIL, 0};
+
+static int check_common(cd_op op, int dt, int64_t n, int64_t ldl, int64_t lda, const cd_opts* opts, int a_dt,
+                        int a_n, int a_ldl, int a_lda, int a_opts) {
+  if (dt != CD_F64 && dt != CD_F32) return -a_dt;
+  if (n < 0 || n > (int64_t(1) << 30)) return -a_n;
+  if (ldl < std::max<int64_t>(1, n)) return -a_ldl;
+  if (lda < std::max<int64_t>(1, n)) return -a_lda;
+  if (opts) {
+    if (opts->nb < 0) return -a_opts;
+    if (opts->route < CD_ROUTE_AUTO || opts->route > CD_ROUTE_SYMBOLIC) return -a_opts;
+    if (opts->out_mode < CD_OUT_TRIL || opts->out_mode > CD_OUT_GRAD) return -a_opts;
+    if (op == CD_OP_FWD && opts->out_mode != CD_OUT_TRIL) return -a_opts;
+    if (opts->flags != 0) return -a_opts;
+  }
+  return 0;
+}
+
+static int route_supported(const cd_opts& o, int64_t n) {
+  if (o.route == CD_ROUTE_SYMBOLIC) return CD_ERR_UNSUPPORTED;
+  (void)n;
+  return 0;
+}
+
+static int strided(cd_op op, cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t sL, void* A, int64_t lda,
+                   int64_t sA, int64_t batch, const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
+                   cd_stream_t stream, bool single) {
+  // argument positions (1-based) in the strided signature / single signature
+  const int pDt = 1, pN = 2, pL = 3, pLdl = 4;
+  const int pSL = single ? 0 : 5, pA = single ? 5 : 6, pLda = single ? 6 : 7, pSA = single ? 0 : 8;
+  const int pB = single ? 0 : 9, pOpts = single ? 7 : 10, pWs = single ? 8 : 11;
+  int r = check_common(op, dt, n, ldl, lda, opts, pDt, pN, pLdl, pLda, pOpts);
+  if (r) return r;
+  if (batch < 0) return -pB;
+  if (n == 0 || batch == 0) return CD_SUCCESS;
+  if (!L) return -pL;
+  if (!A) return -pA;
+  if (batch > 1 && sL < ldl * n) return -pSL;
+  if (batch > 1 && sA < lda * n) return -pSA;
+  const cd_opts o = opts ? *opts : kDefaultOpts;
+  if ((r = route_supported(o, n))) return r;
+  Call k{op, dt, n, batch, Opnd{L, nullptr, sL, ldl, 0}, Opnd{A, nullptr, sA, lda, 0}, o, d_info};
+  return execute(k, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), pWs);
+}
+
+extern "C" {
+
+int cd_chol_rev(cd_dtype dt, int64_t n, const void* L, int64_t ldl, void* Abar, int64_t ldabar, const cd_opts* opts,
+                void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream) {
+  return strided(CD_OP_REV, dt, n, L, ldl, 0, Abar, ldabar, 0, 1, opts, ws, ws_bytes, d_info, stream, true);
+}
+
+int cd_chol_fwd(cd_dtype dt, int64_t n, const void* L, int64_t ldl, void* Adot, int64_t ldadot, const cd_opts* opts,
+                void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream) {
+  return strided(CD_OP_FWD, dt, n, L, ldl, 0, Adot, ldadot, 0, 1, opts, ws, ws_bytes, d_info, stream, true);
+}
+
+int cd_chol_rev_strided_batched(cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t strideL, void* Abar,
+                                int64_t ldabar, int64_t strideAbar, int64_t batch, const cd_opts* opts, void* ws,
+                                size_t ws_bytes, int* d_info, cd_stream_t stream) {
+  return strided(CD_OP_REV, dt, n, L, ldl, strideL, Abar, ldabar, strideAbar, batch, opts, ws, ws_bytes, d_info,
+                 stream, false);
+}
+
+int cd_chol_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t strideL, void* Adot,
+                                int64_t ldadot, int64_t strideAdot, int64_t batch, const cd_opts* opts, void* ws,
+                                size_t ws_bytes, int* d_info, cd_stream_t stream) {
+  return strided(CD_OP_FWD, dt, n, L, ldl, strideL, Adot, ldadot, strideAdot, batch, opts, ws, ws_bytes, d_info,
+                 stream, false);
+}
+
+static int ptr_batched(cd_op op, cd_dtype dt, int64_t n, const void* const* La, int64_t ldl, void* const* Aa,
+                       int64_t lda, int64_t batch, const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
+                       cd_stream_t stream) {
+  int r = check_common(op, dt, n, ldl, lda, opts, 1, 2, 4, 6, 8);
+  if (r) return r;
+  if (batch < 0) return -7;
+  if (n == 0 || batch == 0) return CD_SUCCESS;
+  if (!La) return -3;
+  if (!Aa) return -5;
+  const cd_opts o = opts ? *opts : kDefaultOpts;
+  if ((r = route_supported(o, n))) return r;
+  Call k{op, dt, n, batch, Opnd{nullptr, La, 0, ldl, 0},
+         Opnd{nullptr, reinterpret_cast<const void* const*>(Aa), 0, lda, 0}, o, d_info};
+  return execute(k, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 9);
+}
+
+int cd_chol_rev_batched(cd_dtype dt, int64_t n, const void* const* L_array, int64_t ldl, void* const* Abar_array,
+                        int64_t ldabar, int64_t batch, const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
+                        cd_stream_t stream) {
+  return ptr_batched(CD_OP_REV, dt, n, L_array, ldl, Abar_array, ldabar, batch, opts, ws, ws_bytes, d_info, stream);
+}
+
+int cd_chol_fwd_batched(cd_dtype dt, int64_t n, const void* const* L_array, int64_t ldl, void* const* Adot_array,
+                        int64_t ldadot, int64_t batch, const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
+                        cd_stream_t stream) {
+  return ptr_batched(CD_OP_FWD, dt, n, L_array, ldl, Adot_array, ldadot, batch, opts, ws, ws_bytes, d_info, stream);
+}
+
+size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts) {
+  if ((dt != CD_F64 && dt != CD_F32) || n <= 0 || batch <= 0) return 0;
+  const cd_opts o = opts ? *opts : kDefaultOpts;
+  Call k{op, dt, n, batch, null_opnd(), null_opnd(), o, nullptr};
+  k.L.ld = k.A.ld = n;
+  return plan_size(k);
+}
+
+size_t cd_workspace_size_host(cd_op op, cd_dtype dt, int64_t n, const cd_opts* opts) {
+  const size_t es = dt == CD_F64 ? 8 : 4;
+  const size_t mat = (size_t(n) * n * es + 255) & ~size_t(255);
+  return 2 * mat + cd_workspace_size(op, dt, n, 1, opts);
+}
+
+int cd_chol_host(cd_op op, cd_dtype dt, int64_t n, const void* L_host, void* A_host, const cd_opts* opts, void* ws,
+                 size_t ws_bytes, cd_stream_t stream) {
+  if (op != CD_OP_REV && op != CD_OP_FWD) return -1;
+  if (dt != CD_F64 && dt != CD_F32) return -2;
+  if (n < 0) return -3;
+  if (n == 0) return CD_SUCCESS;
+  if (!L_host) return -4;
+  if (!A_host) return -5;
+  const size_t es = dt == CD_F64 ? 8 : 4;
+  const size_t mat = (size_t(n) * n * es + 255) & ~size_t(255);
+  const size_t need = cd_workspace_size_host(op, dt, n, opts);
+  if (!ws || ws_bytes < need) return -7;
+  char* dL = static_cast<char*>(ws);
+  char* dA = dL + mat;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int r = note_cuda(cudaMemcpyAsync(dL, L_host, size_t(n) * n * es, cudaMemcpyHostToDevice, st));
+  if (r) return r;
+  r = note_cuda(cudaMemcpyAsync(dA, A_host, size_t(n) * n * es, cudaMemcpyHostToDevice, st));
+  if (r) return r;
+  void* ws2 = dA + mat;
+  const size_t ws2b = ws_bytes - 2 * mat;
+  r = (op == CD_OP_REV) ? cd_chol_rev(dt, n, dL, n, dA, n, opts, ws2, ws2b, nullptr, stream)
+                        : cd_chol_fwd(dt, n, dL, n, dA, n, opts, ws2, ws2b, nullptr, stream);
+  if (r) return r;
+  return note_cuda(cudaMemcpyAsync(A_host, dA, size_t(n) * n * es, cudaMemcpyDeviceToHost, st));
+}
+
+const char* cd_status_string(int status) {
+  if (status == CD_SUCCESS) return "success";
+  if (status == CD_ERR_CUDA) return "CUDA error (see cd_last_cuda_error)";
+  if (status == CD_ERR_UNSUPPORTED) return "unsupported combination of valid arguments";
+  if (status < 0) return "invalid argument (-status = 1-based argument position)";
+  return "unknown status";
+}
+
+const char* cd_last_cuda_error(void) { return g_cuda_err; }
+int cd_version(void) { return CD_VERSION; }
+int64_t cd_launch_count(void) { return g_launches; }
+
+void cd_profile_enable(int on) { g_prof.on = on != 0; }
+
+void cd_profile_reset(void) {
+  g_prof.recs.clear();
+  g_prof.used = 0;
+}
+
+int cd_profile_read(int cls, double* ms, double* flops, int64_t* launches) {
+  double t = 0.0, f = 0.0;
+  int64_t cnt = 0;
+  for (const ProfRec& r : g_prof.recs) {
+    if (r.cls != cls) continue;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return note_cuda(e);
+    float x = 0.f;
+    e = cudaEventElapsedTime(&x, r.a, r.b);
+    if (e != cudaSuccess) return note_cuda(e);
+    t += x;
+    f += r.flops;
+    ++cnt;
+  }
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  if (launches) *launches = cnt;
+  return CD_SUCCESS;
+}
+void cd_reset_launch_count(void) { g_launches = 0; }
+
+}  // extern "C"

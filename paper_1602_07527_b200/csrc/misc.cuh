@@ -1,0 +1,144 @@
+// misc.cuh -- small kernels of the blocked sweeps: diagonal-block inverses (the panel
+// solves C D^{-1} / C D^{-T} of PAPER.md:695, 664 become GEMMs with D^{-1}), copies,
+// output-convention epilogues (Eq. 9 mirror / GRAD) and status.
+#pragma once
+#include "common.cuh"
+
+namespace cd {
+
+// Partition of [0, n) into diagonal blocks of width nb.
+//   reverse: the short block (n mod nb) is the FIRST one
+//   forward: the short block is the LAST one
+__host__ __device__ inline int nblocks(int n, int nb) { return (n + nb - 1) / nb; }
+__host__ __device__ inline void block_range(int n, int nb, bool reverse, int q, int& j0, int& w) {
+  const int r = n % nb;
+  if (!reverse || r == 0) {
+    j0 = q * nb;
+    w = min(nb, n - j0);
+  } else if (q == 0) {
+    j0 = 0;
+    w = r;
+  } else {
+    j0 = r + (q - 1) * nb;
+    w = nb;
+  }
+}
+
+constexpr int TRINV_THREADS = 512;
+constexpr int CTA_NMAX_TRINV = 128;  // widest diagonal block inverted on chip
+
+// Dinv[b][q] = inverse of tril(L[j0:j0+w, j0:j0+w]), dense w x w (ld = ldi), upper zero.
+// Column c of X = D^{-1} solves D x = e_c by forward substitution; one warp per column,
+// lanes own rows, x_t broadcast with a shuffle.  grid = (nblk, batch).
+template <typename T>
+__global__ void __launch_bounds__(TRINV_THREADS)
+    k_trinv(int n, int nb, int reverse, Opnd Ld, T* __restrict__ Dinv, int64_t ldi, int64_t stride_blk) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sD = reinterpret_cast<T*>(smem_raw);
+  const int q = blockIdx.x;
+  const int64_t b = blockIdx.y;
+  int j0, w;
+  block_range(n, nb, reverse != 0, q, j0, w);
+  const T* L = optr<T>(Ld, b);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int m = warp; m < w; m += nw) {
+    const int cs = tri_col(w, m);
+    for (int i = m + lane; i < w; i += 32)
+      cp_async_zfill<sizeof(T)>(sD + cs + i - m, L + (j0 + i) + int64_t(j0 + m) * Ld.ld, true);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  T* X = Dinv + (int64_t(b) * gridDim.x + q) * stride_blk;
+  for (int c = warp; c < w; c += nw) {
+    T x[CTA_NMAX_TRINV / 32];
+    // rhs = e_c restricted to rows >= c; rows r = c + lane + 32u
+#pragma unroll
+    for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u) x[u] = (lane == 0 && u == 0) ? T(1) : T(0);
+    for (int t = c; t < w; ++t) {
+      const int u_t = (t - c) >> 5, l_t = (t - c) & 31;
+      T xt = T(0);
+#pragma unroll
+      for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u)
+        if (u == u_t) xt = x[u];
+      xt = __shfl_sync(0xffffffffu, xt, l_t) / sD[tri_col(w, t)];
+#pragma unroll
+      for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u) {
+        const int r = c + lane + 32 * u;
+        if (u == u_t && lane == l_t) x[u] = xt;
+        else if (r > t && r < w) x[u] -= sD[tri_col(w, t) + r - t] * xt;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u) {
+      const int r = c + lane + 32 * u;
+      if (r < w) X[r + int64_t(c) * ldi] = x[u];
+    }
+    for (int r = lane; r < c; r += 32) X[r + int64_t(c) * ldi] = T(0);
+  }
+}
+
+// D(i, j) = S(i, j), M x N per batch entry.
+template <typename T>
+__global__ void k_copy(int M, int N, int64_t batch, Opnd S, Opnd D) {
+  const int64_t MN = int64_t(M) * N, total = MN * batch;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(idx % M), c = int((idx / M) % N);
+    const int64_t b = idx / MN;
+    optr_w<T>(D, b)[r + int64_t(c) * D.ld] = optr<T>(S, b)[r + int64_t(c) * S.ld];
+  }
+}
+
+// S = tril(A) + tril(A)^T (diagonal doubled), dense n x n; or (clean=1) S = tril(A), upper 0.
+template <typename T>
+__global__ void k_sym2(int n, int64_t batch, Opnd A, Opnd S, int clean) {
+  const int64_t nn = int64_t(n) * n, total = nn * batch;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(idx % n), m = int((idx / n) % n);
+    const int64_t b = idx / nn;
+    const T* a = optr<T>(A, b);
+    T v;
+    if (clean) v = (i >= m) ? a[i + int64_t(m) * A.ld] : T(0);
+    else if (i > m) v = a[i + int64_t(m) * A.ld];
+    else if (i < m) v = a[m + int64_t(i) * A.ld];
+    else v = T(2) * a[i + int64_t(i) * A.ld];
+    optr_w<T>(S, b)[i + int64_t(m) * S.ld] = v;
+  }
+}
+
+// Output convention epilogue on the full n x n matrix (mode 1 SYM: mirror lower to
+// upper; mode 2 GRAD: halve lower off-diagonals, then mirror).
+template <typename T>
+__global__ void k_out_mode(int n, int64_t batch, Opnd A, int mode) {
+  const int64_t nn = int64_t(n) * n, total = nn * batch;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(idx % n), m = int((idx / n) % n);
+    if (i <= m) continue;
+    const int64_t b = idx / nn;
+    T* a = optr_w<T>(A, b);
+    T v = a[i + int64_t(m) * A.ld];
+    if (mode == 2) {
+      v *= T(0.5);
+      a[i + int64_t(m) * A.ld] = v;
+    }
+    a[m + int64_t(i) * A.ld] = v;
+  }
+}
+
+// info[b] = first 1-based j with L[j-1, j-1] zero or non-finite, else 0.  One CTA per matrix.
+template <typename T>
+__global__ void k_diag_info(int n, Opnd Ld, int* __restrict__ info) {
+  __shared__ int sbad;
+  if (threadIdx.x == 0) sbad = 0x7fffffff;
+  __syncthreads();
+  const int64_t b = blockIdx.x;
+  const T* L = optr<T>(Ld, b);
+  for (int j = threadIdx.x; j < n; j += blockDim.x)
+    if (bad_pivot(L[j + int64_t(j) * Ld.ld])) atomicMin(&sbad, j + 1);
+  __syncthreads();
+  if (threadIdx.x == 0) info[b] = (sbad == 0x7fffffff) ? 0 : sbad;
+}
+
+}  // namespace cd

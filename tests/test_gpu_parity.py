@@ -1,0 +1,181 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element on the same seeded inputs (tolerances: north star -- max relative error
+normalised by ||tril(ref)||_F <= 1e-10 fp64, <= 1e-4 fp32)."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1602_07527_b200 as cd
+import synthetic
+from gpu_helpers import fp32_round, nerr, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+TOL64, TOL32 = 1e-10, 1e-4
+
+SIZES = [1, 2, 3, 5, 8, 16, 31, 32, 33, 47, 63, 64, 65, 100, 127, 128, 129, 200, 255, 256, 257, 300, 517]
+
+
+def oracle_rev(L, Lb):
+    return np.stack([oracle.chol_rev(L[b], Lb[b]) for b in range(L.shape[0])]) if L.ndim == 3 else oracle.chol_rev(L, Lb)
+
+
+def oracle_fwd(L, Sd):
+    if L.ndim == 3:
+        return np.stack([oracle.chol_fwd(L[b], np.tril(Sd[b])) for b in range(L.shape[0])])
+    return oracle.chol_fwd(L, np.tril(Sd))
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_rev_single_f64(n):
+    L, Lb, _ = synthetic.draw(n, n)
+    out = cd.chol_rev(to_dev(L), to_dev(Lb))
+    assert nerr(to_host(out), oracle.chol_rev(L, Lb)) < TOL64
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_fwd_single_f64(n):
+    L, _, Sd = synthetic.draw(n, 1000 + n, sdot=True)
+    out = cd.chol_fwd(to_dev(L), to_dev(np.tril(Sd)))
+    assert nerr(to_host(out), oracle_fwd(L, Sd)) < TOL64
+
+
+@pytest.mark.parametrize("n,nb", [(300, 1), (300, 2), (300, 3), (300, 7), (300, 16), (300, 32), (300, 33),
+                                  (300, 64), (300, 100), (300, 128), (129, 128), (160, 31)])
+def test_nb_sweep(n, nb):
+    # any partition; SPEC.md:301 nb-invariance
+    L, Lb, Sd = synthetic.draw(n, 77, sdot=True)
+    r = cd.chol_rev(to_dev(L), to_dev(Lb), nb=nb)
+    assert nerr(to_host(r), oracle.chol_rev(L, Lb)) < TOL64
+    f = cd.chol_fwd(to_dev(L), to_dev(np.tril(Sd)), nb=nb)
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
+
+
+def test_nb_too_large_is_unsupported():
+    L, Lb, _ = synthetic.draw(300, 1)
+    with pytest.raises(cd.CholdiffError):
+        cd.chol_rev(to_dev(L), to_dev(Lb), nb=256)
+
+
+@pytest.mark.parametrize("n", [17, 64, 200])
+@pytest.mark.parametrize("pad", [1, 3])
+def test_leading_dimension(n, pad):
+    L, Lb, Sd = synthetic.draw(n, 5 * n + pad, sdot=True)
+    Ld, Ad = to_dev(L, ld_pad=pad), to_dev(Lb, ld_pad=pad)
+    assert Ld.stride(-1) == n + pad
+    out = cd.chol_rev(Ld, Ad)
+    assert out.data_ptr() == Ad.data_ptr()  # in place
+    assert nerr(to_host(out), oracle.chol_rev(L, Lb)) < TOL64
+    f = cd.chol_fwd(to_dev(L, ld_pad=pad), to_dev(np.tril(Sd), ld_pad=pad))
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
+
+
+@pytest.mark.parametrize("n", [1, 5, 17, 32, 33, 64, 100, 128, 150])
+def test_strided_batched(n):
+    B = 37 if n <= 128 else 5
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=3 * n, sdot=True)
+    r = cd.chol_rev(to_dev(L), to_dev(Lb))
+    assert nerr(to_host(r), oracle_rev(L, Lb)) < TOL64
+    f = cd.chol_fwd(to_dev(L), to_dev(np.tril(Sd)))
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
+
+
+@pytest.mark.parametrize("n", [9, 32, 96, 140])
+def test_pointer_array_batched(n):
+    B = 6
+    L, Lb, _ = synthetic.draw_batch(n, B, seed=n)
+    Ls = [to_dev(L[b]) for b in range(B)]
+    As = [to_dev(Lb[b]) for b in range(B)]
+    lp = torch.tensor([t.data_ptr() for t in Ls], dtype=torch.int64, device="cuda")
+    ap = torch.tensor([t.data_ptr() for t in As], dtype=torch.int64, device="cuda")
+    nbytes = cd.workspace_size("rev", torch.float64, n, B)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+    rc = cd.lib().cd_chol_rev_batched(0, n, lp.data_ptr(), n, ap.data_ptr(), n, B, None, ws.data_ptr(), nbytes,
+                                      None, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    out = np.stack([to_host(a) for a in As])
+    assert nerr(out, oracle_rev(L, Lb)) < TOL64
+
+
+@pytest.mark.parametrize("n", [1, 7, 32, 33, 100, 128, 200, 512])
+def test_f32_vs_oracle_on_rounded_inputs(n):
+    B = 4
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=11 * n, sdot=True)
+    L, Lb, Sd = fp32_round(L, Lb, Sd)
+    r = cd.chol_rev(to_dev(L, torch.float32), to_dev(Lb, torch.float32))
+    assert nerr(to_host(r), oracle_rev(L, Lb)) < TOL32
+    f = cd.chol_fwd(to_dev(L, torch.float32), to_dev(np.tril(Sd), torch.float32))
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL32
+
+
+@pytest.mark.parametrize("n", [6, 32, 90, 260])
+def test_out_modes(n):
+    L, Lb, _ = synthetic.draw(n, 400 + n)
+    sym = oracle.chol_rev_symbolic_sym(L, Lb)  # Eq. 9
+    o_sym = to_host(cd.chol_rev(to_dev(L), to_dev(Lb), out="sym"))
+    assert np.array_equal(o_sym, o_sym.T)
+    assert np.abs(o_sym - sym).max() / np.linalg.norm(sym) < TOL64
+    G = 0.5 * (sym + np.diag(np.diag(sym)))  # G = (S + S^T)/2: Eq. 9 with off-diagonals halved
+    o_g = to_host(cd.chol_rev(to_dev(L), to_dev(Lb), out="grad"))
+    assert np.array_equal(o_g, o_g.T)
+    assert np.abs(o_g - G).max() / np.linalg.norm(G) < TOL64
+
+
+@pytest.mark.parametrize("n", [5, 32, 70, 300])
+def test_upper_triangle_never_read_nor_written(n):
+    L, Lb, Sd = synthetic.draw(n, 9 + n, sdot=True)
+    Lp, Ap = synthetic.poison_upper(L), synthetic.poison_upper(Lb)
+    out = to_host(cd.chol_rev(to_dev(Lp), to_dev(Ap)))
+    iu = np.triu_indices(n, 1)
+    assert np.all(np.isnan(out[iu]))
+    assert nerr(out, oracle.chol_rev(L, Lb)) < TOL64
+    f = to_host(cd.chol_fwd(to_dev(Lp), to_dev(synthetic.poison_upper(np.tril(Sd)))))
+    assert np.all(np.isnan(f[iu]))
+    assert nerr(f, oracle_fwd(L, Sd)) < TOL64
+
+
+@pytest.mark.parametrize("n", [4, 32, 64, 300])
+def test_info_reports_singular_factor(n):
+    B = 3
+    L, Lb, _ = synthetic.draw_batch(n, B, seed=1)
+    L[1, n // 2, n // 2] = 0.0
+    _, info = cd.chol_rev(to_dev(L), to_dev(Lb), info=True)
+    assert info.cpu().tolist() == [0, n // 2 + 1, 0]
+    _, info = cd.chol_fwd(to_dev(L), to_dev(np.tril(Lb)), info=True)
+    assert info.cpu().tolist() == [0, n // 2 + 1, 0]
+
+
+def test_zero_sizes():
+    e = torch.empty(0, 0, dtype=torch.float64, device="cuda")
+    cd.chol_rev(e, e.clone())
+    eb = torch.empty(0, 4, 4, dtype=torch.float64, device="cuda")
+    cd.chol_rev(eb, eb.clone())
+
+
+@pytest.mark.parametrize("n", [32, 64, 300])
+def test_power_of_two_scaling_bit_exact(n):
+    # property holding at any size for a deterministic kernel
+    L, Lb, _ = synthetic.draw(n, 123)
+    a = to_host(cd.chol_rev(to_dev(L), to_dev(Lb)))
+    b = to_host(cd.chol_rev(to_dev(L * 4.0), to_dev(Lb)))
+    c = to_host(cd.chol_rev(to_dev(L), to_dev(Lb * 0.125)))
+    assert np.array_equal(np.tril(b), np.tril(a) * 0.25)
+    assert np.array_equal(np.tril(c), np.tril(a) * 0.125)
+
+
+def test_deterministic():
+    L, Lb, _ = synthetic.draw(700, 3)
+    a = to_host(cd.chol_rev(to_dev(L), to_dev(Lb)))
+    b = to_host(cd.chol_rev(to_dev(L), to_dev(Lb)))
+    assert np.array_equal(np.tril(a), np.tril(b))
+
+
+def test_host_buffer_path():
+    n = 300
+    L, Lb, _ = synthetic.draw(n, 8)
+    Lh = torch.from_numpy(synthetic.to_colmajor(L)).transpose(0, 1).pin_memory()
+    Ah = torch.from_numpy(synthetic.to_colmajor(Lb)).transpose(0, 1).pin_memory()
+    cd.chol_host("rev", Lh, Ah)
+    assert nerr(Ah.numpy(), oracle.chol_rev(L, Lb)) < TOL64
