@@ -12,6 +12,8 @@
 // Workspace: every driver runs in two modes, "plan" (no launches, only workspace
 // carving) and "run"; cd_workspace_size returns the plan's high-water mark, so the
 // size query and the launch sequence can never disagree.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,9 +25,11 @@
 #include "../../include/choldiff.h"
 #include "common.cuh"
 #include "gemm.cuh"
+#include "gemm_tma.cuh"
 #include "misc.cuh"
 #include "sweep_cta.cuh"
 #include "sweep_warp.cuh"
+#include "sweep_dmma32.cuh"
 
 namespace cd {
 
@@ -97,6 +101,50 @@ static int grid_1d(int64_t total, int threads, int sms) {
 template <typename K>
 static void set_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+// ------------------------------------------------------------------ TMA tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static bool g_tma_disabled = getenv("CD_DISABLE_TMA") != nullptr;
+
+// 2-D (or 3-D with batch) fp64 tensor map over a column-major view of `rows` x `cols`
+// elements starting at element pointer `p` (leading dimension ld, batch stride bstride).
+// `shift` (kept for the kernel's coordinate arithmetic) is always 0.
+static bool make_tmap(CUtensorMap* map, int* shift, const void* p, int64_t rows, int64_t cols, int64_t ld,
+                      int64_t bstride, int64_t batch, int box0, int box1) {
+  auto enc = tmap_encoder();
+  if (!enc || rows <= 0 || cols <= 0) return false;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(p);
+  // The view must start on a 16-byte boundary: a map whose base was moved down and a
+  // box starting at an odd element faulted (cudaErrorIllegalInstruction) on B200 /
+  // driver 580 in testing; such views (odd block boundaries) use the cp.async kernel.
+  if (addr % 16) return false;
+  const int sh = 0;
+  if ((ld * 8) % 16 || (batch > 1 && (bstride * 8) % 16)) return false;
+  const void* base = reinterpret_cast<const char*>(p) - sh * 8;
+  cuuint64_t dims[3] = {cuuint64_t(rows + sh), cuuint64_t(cols), cuuint64_t(std::max<int64_t>(batch, 1))};
+  cuuint64_t strides[2] = {cuuint64_t(ld * 8), cuuint64_t(std::max<int64_t>(bstride, 1) * 8)};
+  cuuint32_t box[3] = {cuuint32_t(box0), cuuint32_t(box1), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const cuuint32_t rank = batch > 1 ? 3 : 2;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  *shift = sh;
+  return r == CUDA_SUCCESS;
 }
 
 // ------------------------------------------------------------------ GEMM launcher
@@ -186,7 +234,43 @@ struct Gemm {
     kern<<<grid, G_THREADS, GemmLayout<T, A_, B_>::SMEM, c.st>>>(p);
     c.launched();
   }
+  // TMA-fed warp-specialised kernel (fp64, strided operands with even ld)
+  bool build_maps(TmaMaps& tm) {
+    if (sizeof(T) != 8 || g_tma_disabled) return false;
+    tm.batched = p.batch > 1 ? 1 : 0;
+    for (int s = 0; s < p.nseg; ++s) {
+      const GemmSeg& sg = p.seg[s];
+      if (sg.A.arr || sg.B.arr) return false;
+      const T* pa = static_cast<const T*>(sg.A.base) + sg.A.off;
+      const T* pb = static_cast<const T*>(sg.B.base) + sg.B.off;
+      const bool okA = TA == 0 ? make_tmap(&tm.a[s], &tm.a_shift[s], pa, p.M, sg.K, sg.A.ld, sg.A.stride, p.batch, 132, 16)
+                               : make_tmap(&tm.a[s], &tm.a_shift[s], pa, sg.K, p.M, sg.A.ld, sg.A.stride, p.batch, 20, 128);
+      const bool okB = TB == 0 ? make_tmap(&tm.b[s], &tm.b_shift[s], pb, sg.K, p.N, sg.B.ld, sg.B.stride, p.batch, 20, 128)
+                               : make_tmap(&tm.b[s], &tm.b_shift[s], pb, p.N, sg.K, sg.B.ld, sg.B.stride, p.batch, 132, 16);
+      if (!okA || !okB) return false;
+    }
+    return true;
+  }
+  template <int A_, int B_>
+  bool launch_tma(dim3 grid) {
+    TmaMaps tm;
+    memset(&tm, 0, sizeof(tm));
+    if (!build_maps(tm)) return false;
+    auto kern = k_gemm_tma<A_, B_>;
+    set_smem(kern, TmaLayout<A_, B_>::SMEM);
+    kern<<<grid, TG_THREADS, TmaLayout<A_, B_>::SMEM, c.st>>>(p, tm);
+    c.launched();
+    return true;
+  }
   void launch(dim3 grid) {
+    if constexpr (sizeof(T) == 8) {
+      bool done = false;
+      if (TA == 0 && TB == 0) done = launch_tma<0, 0>(grid);
+      else if (TA == 0 && TB == 1) done = launch_tma<0, 1>(grid);
+      else if (TA == 1 && TB == 0) done = launch_tma<1, 0>(grid);
+      else done = launch_tma<1, 1>(grid);
+      if (done) return;
+    }
     if (TA == 0 && TB == 0) launch_t<0, 0>(grid);
     else if (TA == 0 && TB == 1) launch_t<0, 1>(grid);
     else if (TA == 1 && TB == 0) launch_t<1, 0>(grid);
@@ -215,7 +299,23 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
   if (n <= 32) {
     const size_t smem = sweep_warp_smem<T>();
     const unsigned grid = unsigned((batch + SW_WPB - 1) / SW_WPB);
-    if (rev) {
+    if (rev && sizeof(T) == 8) {
+      // fp64 reverse: blocked N_b = 8 sweep on DMMA tiles (sweep_dmma32.cuh)
+      const size_t sm2 = dmma32_smem();
+      // persistent grid: enough CTAs for every SM's shared-memory-limited residency
+      const int per_sm = std::max<int>(1, int((227 * 1024) / (sm2 + 1024)));
+      const unsigned g2 = unsigned(std::min<int64_t>((batch + D32_WPB - 1) / D32_WPB, int64_t(c.sms) * per_sm));
+      const Opnd Lo = L, Ao = A;
+      auto go = [&](auto kern) {
+        set_smem(kern, sm2);
+        kern<<<g2, D32_WPB * 32, sm2, c.st>>>(n, batch, Lo, Ao, out_mode, info);
+      };
+      const int nblk = (n + 7) / 8;
+      if (nblk == 1) go(k_rev_dmma32<1>);
+      else if (nblk == 2) go(k_rev_dmma32<2>);
+      else if (nblk == 3) go(k_rev_dmma32<3>);
+      else go(k_rev_dmma32<4>);
+    } else if (rev) {
       set_smem(k_sweep_warp_rev<T>, smem);
       k_sweep_warp_rev<T><<<grid, SW_WPB * 32, smem, c.st>>>(n, batch, L, A, out_mode, info);
     } else {
@@ -233,7 +333,7 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
     const size_t smem = sweep_cta_smem<T>(n);
     if (rev) {
       set_smem(k_sweep_cta_rev<T>, smem);
-      k_sweep_cta_rev<T><<<unsigned(batch), CTA_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+      k_sweep_cta_rev<T><<<unsigned(batch), CTA_REV_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
     } else {
       set_smem(k_sweep_cta_fwd<T>, smem);
       k_sweep_cta_fwd<T><<<unsigned(batch), CTA_THREADS, smem, c.st>>>(n, L, A, S, info);

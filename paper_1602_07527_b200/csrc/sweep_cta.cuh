@@ -22,12 +22,13 @@
 namespace cd {
 
 constexpr int CTA_NMAX = 128;
-constexpr int CTA_THREADS = 512;
+constexpr int CTA_THREADS = 512;      // forward sweep
+constexpr int CTA_REV_THREADS = 1024; // reverse sweep: 8 threads per column m
 
 template <typename T>
 inline size_t sweep_cta_smem(int n) {
   const size_t tri = size_t(n) * (n + 1) / 2;
-  return 2 * tri * sizeof(T) + 4 * sizeof(T) + 16;
+  return 2 * tri * sizeof(T) + (CTA_NMAX + 8) * sizeof(T) + 16;
 }
 
 template <typename T>
@@ -62,99 +63,152 @@ __device__ __forceinline__ void cta_write_sym2(T* S, int64_t lds, int n, const T
   }
 }
 
+// Row-major packed lower triangle: row i holds (i, 0..i) at i(i+1)/2.
+__device__ __forceinline__ int tri_row(int i) { return (i * (i + 1)) >> 1; }
+
 template <typename T>
-__global__ void __launch_bounds__(CTA_THREADS)
+__device__ __forceinline__ void cta_stage_rows(const T* __restrict__ g, int64_t ld, int n, T* s, int warp, int lane,
+                                               int nw) {
+  for (int m = warp; m < n; m += nw)
+    for (int i = m + lane; i < n; i += 32) cp_async_zfill<sizeof(T)>(s + tri_row(i) + m, g + i + int64_t(m) * ld, true);
+}
+
+// Reverse sweep, one CTA (8 threads per column m of the rank-1 / GEMV updates).
+// Column j's values are kept UNSCALED (u = Abar[j+1:n, j]) while in use; with rd = 1/d:
+//   dbar   = (dbar - (c^T u) rd) rd
+//   rbar_m -= dbar L(j,m) + rd * sum_i u_i L(i,m)                     (574)
+//   Bbar(i,m) -= u_i * (rd L(j,m))                                    (575)
+//   Abar(j,j) = dbar / 2                                              (576)
+// and cbar = u * rd is applied to every column once, at the end.  The threads
+// (8) that own column m = j-1 fold the NEXT column's dot product c^T u into their
+// update loop, so each column costs a single __syncthreads().
+template <typename T>
+__global__ void __launch_bounds__(CTA_REV_THREADS)
     k_sweep_cta_rev(int n, Opnd Ld, Opnd Ad, int out_mode, Opnd Sd, int* __restrict__ info) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tri = n * (n + 1) / 2;
   T* sL = reinterpret_cast<T*>(smem_raw);
   T* sA = sL + tri;
-  T* sdb = sA + tri;  // [2] dbar (before halving) of the current / next column
+  T* sRd = sA + tri;                 // [n] 1 / L_jj
+  T* sdb = sRd + CTA_NMAX;           // [2] dbar (before halving)
   int* sbad = reinterpret_cast<int*>(sdb + 4);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int64_t b = blockIdx.x;
   const T* L = optr<T>(Ld, b);
   T* A = optr_w<T>(Ad, b);
 
-  if (threadIdx.x == 0) *sbad = 0x7fffffff;
-  cta_stage<T>(L, Ld.ld, n, sL, warp, lane, nw);
-  cta_stage<T>(A, Ad.ld, n, sA, warp, lane, nw);
+  if (tid == 0) *sbad = 0x7fffffff;
+  cta_stage_rows<T>(L, Ld.ld, n, sL, warp, lane, nw);
+  cta_stage_rows<T>(A, Ad.ld, n, sA, warp, lane, nw);
   cp_async_wait_all();
   __syncthreads();
-  cta_info<T>(sL, n, sbad, info, b);
-
-  // column n-1: no cbar; dbar <- dbar/d, then /2
-  if (threadIdx.x == 0) {
-    const int cs = tri_col(n, n - 1);
-    const T db = sA[cs] / sL[cs];
-    sA[cs] = db * T(0.5);
+  for (int t = tid; t < n; t += blockDim.x) {
+    const T d = sL[tri_row(t) + t];
+    if (bad_pivot(d)) atomicMin(sbad, t + 1);
+    sRd[t] = T(1) / d;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (info) info[b] = (*sbad == 0x7fffffff) ? 0 : *sbad;
+    const int c = tri_row(n - 1) + n - 1;  // column n-1: no cbar
+    const T db = sA[c] * sRd[n - 1];
+    sA[c] = db * T(0.5);
     sdb[(n - 1) & 1] = db;
   }
   __syncthreads();
 
+  const int m = tid >> 3, q = tid & 7;
   for (int j = n - 1; j >= 1; --j) {
-    const int csj = tri_col(n, j);
-    const T dbar = sdb[j & 1];
-    T cb[CTA_NMAX / 32];
+    if ((warp << 2) < j) {  // warp owns columns m = 4*warp .. 4*warp+3
+      const bool act = m < j;
+      const T dbar = sdb[j & 1];
+      const T rdj = sRd[j];
+      const T Ljm = act ? sL[tri_row(j) + m] : T(0);
+      const T wgt = rdj * Ljm;
+      const bool nxt = (m == j - 1);
+      T acc = T(0), sj = T(0);
+      if (act) {
+        // rows i = j+1+q, +8, ...; batches of 4 rows with all loads issued first
+        for (int i0 = j + 1 + q; i0 < n; i0 += 32) {
+          T u[4], Lm[4], a[4];
+          int ro[4];
 #pragma unroll
-    for (int u = 0; u < CTA_NMAX / 32; ++u) {
-      const int i = j + 1 + lane + 32 * u;
-      cb[u] = (i < n) ? sA[csj + i - j] : T(0);
-    }
-    // largest m <= j-1 owned by this warp (owner of m is m % nw)
-    const int jm1 = j - 1;
-    const int mtop = jm1 - (((jm1 - warp) % nw) + nw) % nw;
-    for (int m = mtop; m >= 0; m -= nw) {
-      const int csm = tri_col(n, m);
-      const T r_m = sL[csm + j - m];  // L(j, m)
-      T acc = T(0);
+          for (int k = 0; k < 4; ++k) {
+            const int i = i0 + 8 * k;
+            ro[k] = tri_row(i);
+            const bool ok = i < n;
+            u[k] = ok ? sA[ro[k] + j] : T(0);
+            Lm[k] = ok ? sL[ro[k] + m] : T(0);
+            a[k] = ok ? sA[ro[k] + m] : T(0);
+          }
 #pragma unroll
-      for (int u = 0; u < CTA_NMAX / 32; ++u) {
-        const int i = j + 1 + lane + 32 * u;
-        if (i < n) {
-          acc += cb[u] * sL[csm + i - m];           // [cbar^T] B
-          sA[csm + i - m] -= cb[u] * r_m;          // Bbar <- Bbar - cbar r
+          for (int k = 0; k < 4; ++k) {
+            acc += u[k] * Lm[k];
+            a[k] -= u[k] * wgt;                  // Bbar <- Bbar - cbar r
+            if (nxt) sj += Lm[k] * a[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (i0 + 8 * k < n) sA[ro[k] + m] = a[k];
         }
       }
-      acc = warp_sum(acc);
-      if (lane == 0) sA[csm + j - m] -= dbar * r_m + acc;  // rbar <- rbar - [dbar cbar^T][r;B] (574)
-      if (m == jm1) {
-        // next column (j-1): dbar <- dbar - c^T cbar/d; [dbar;cbar] /= d; dbar/2 (572-573, 576)
-        __syncwarp();
-        const int jj = jm1;
-        T s = T(0);
-        for (int i = jj + 1 + lane; i < n; i += 32) s += sL[csm + i - jj] * sA[csm + i - jj];
-        s = warp_sum(s);
-        const T rd = T(1) / sL[csm];
-        const T db = (sA[csm] - s * rd) * rd;
-        for (int i = jj + 1 + lane; i < n; i += 32) sA[csm + i - jj] *= rd;
-        if (lane == 0) {
-          sA[csm] = db * T(0.5);
-          sdb[jj & 1] = db;
-        }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      T r = T(0);
+      if (act && q == 0) {                       // rbar <- rbar - [dbar cbar^T][r;B]
+        r = sA[tri_row(j) + m] - (dbar * Ljm + rdj * acc);
+        sA[tri_row(j) + m] = r;
+      }
+      sj += __shfl_xor_sync(0xffffffffu, sj, 1);
+      sj += __shfl_xor_sync(0xffffffffu, sj, 2);
+      sj += __shfl_xor_sync(0xffffffffu, sj, 4);
+      r = __shfl_sync(0xffffffffu, r, lane & ~7);
+      if (nxt && q == 0) {
+        // next column j-1:  s = c^T u over rows j..n-1 (row j is the new rbar)
+        const T s = sj + Ljm * r;
+        const T rdm = sRd[m];
+        const int dg = tri_row(m) + m;
+        const T db = (sA[dg] - s * rdm) * rdm;
+        sA[dg] = db * T(0.5);
+        sdb[m & 1] = db;
       }
     }
     __syncthreads();
   }
-
-  // write back tril (and the requested mirror) ; optional S for the blocked driver
-  for (int m = warp; m < n; m += nw) {
-    const int cs = tri_col(n, m);
-    for (int i = m + lane; i < n; i += 32) {
-      T v = sA[cs + i - m];
-      if (out_mode == 2 && i != m) v *= T(0.5);
-      A[i + int64_t(m) * Ad.ld] = v;
-    }
+  // cbar = u * rd for every column (strict lower part)
+  for (int e = tid; e < tri; e += blockDim.x) {
+    // row i = floor((sqrt(8e+1)-1)/2), col = e - i(i+1)/2
+    int i = int((sqrtf(8.f * e + 1.f) - 1.f) * 0.5f);
+    while (tri_row(i + 1) <= e) ++i;
+    while (tri_row(i) > e) --i;
+    const int c = e - tri_row(i);
+    if (i > c) sA[e] *= sRd[c];
   }
+  __syncthreads();
+
+  for (int mm = warp; mm < n; mm += nw)
+    for (int i = mm + lane; i < n; i += 32) {
+      T v = sA[tri_row(i) + mm];
+      if (out_mode == 2 && i != mm) v *= T(0.5);
+      A[i + int64_t(mm) * Ad.ld] = v;
+    }
   if (out_mode != 0) {
-    for (int i = warp; i < n; i += nw)      // global column i, upper rows m < i
-      for (int m = lane; m < i; m += 32) {
-        T v = sA[tri_col(n, m) + i - m];
+    for (int i = warp; i < n; i += nw)  // global column i, upper rows mm < i
+      for (int mm = lane; mm < i; mm += 32) {
+        T v = sA[tri_row(i) + mm];
         if (out_mode == 2) v *= T(0.5);
-        A[m + int64_t(i) * Ad.ld] = v;
+        A[mm + int64_t(i) * Ad.ld] = v;
       }
   }
-  if (Sd.base || Sd.arr) cta_write_sym2<T>(optr_w<T>(Sd, b), Sd.ld, n, sA);
+  if (Sd.base || Sd.arr) {  // S = Dbar + Dbar^T (diagonal doubled), dense
+    T* S = optr_w<T>(Sd, b);
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int i = e % n, c = e / n;
+      const T v = (i >= c) ? sA[tri_row(i) + c] : sA[tri_row(c) + i];
+      S[i + int64_t(c) * Sd.ld] = (i == c) ? T(2) * v : v;
+    }
+  }
 }
 
 // Forward. Optionally writes a clean dense copy of tril(Ldot) (upper zero) to Dd,
