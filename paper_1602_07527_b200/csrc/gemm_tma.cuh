@@ -151,9 +151,13 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_gemm_tma(const GemmParams p, 
   // ---------------- consumers ----------------
   const int wm = warp >> 2, wn = warp & 3, g = lane >> 2, t = lane & 3;
   double acc[8][4][2];
-  const bool pre = p.splits == 1 && p.beta != 0.0 && (p.alpha == 1.0 || p.alpha == -1.0);
+  // D = Cin - sum (alpha = -1, beta = 1) or Cin + sum (alpha = 1, beta = 1): the
+  // accumulators start as Cin (raw global loads straight into the accumulator
+  // registers, all independent, overlapping the TMA prologue) and the sign of the
+  // sum is carried by the B fragments; the epilogue is then pure stores.
+  const bool pre = p.splits == 1 && p.beta == 1.0 && (p.alpha == 1.0 || p.alpha == -1.0);
+  const double bsign = pre ? p.alpha : 1.0;
   {
-    const double sc = pre ? p.beta / p.alpha : 0.0;
     const double* Cp = pre ? optr<double>(p.Cin, b) : nullptr;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_gemm_tma(const GemmParams p, 
         for (int e = 0; e < 2; ++e) {
           const int r = m0 + wm * 64 + i * 8 + g;
           const int c = n0 + wn * 32 + j * 8 + 2 * t + e;
-          acc[i][j][e] = (pre && r < p.M && c < p.N) ? sc * Cp[r + int64_t(c) * p.Cin.ld] : 0.0;
+          acc[i][j][e] = (pre && r < p.M && c < p.N) ? __ldcg(Cp + r + int64_t(c) * p.Cin.ld) : 0.0;
         }
   }
 
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_gemm_tma(const GemmParams p, 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int n = wn * 32 + j * 8 + g;
-        bb[j] = Lay::B_KN ? bs[k * Lay::B_PITCH + n] : bs[n * Lay::B_PITCH + k];
+        bb[j] = bsign * (Lay::B_KN ? bs[k * Lay::B_PITCH + n] : bs[n * Lay::B_PITCH + k]);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -210,11 +214,13 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_gemm_tma(const GemmParams p, 
         const int c = n0 + wn * 32 + j * 8 + 2 * t + e;
         if (r < p.M && c < p.N && (!p.tril || r >= c)) {
           if (part) {
-            part[r + int64_t(c) * p.M] = acc[i][j][e];
+            __stcg(part + r + int64_t(c) * p.M, acc[i][j][e]);
+          } else if (pre) {
+            __stcg(D + r + int64_t(c) * p.D.ld, acc[i][j][e]);
           } else {
             double v = alpha * acc[i][j][e];
-            if (Cin) v += beta * Cin[r + int64_t(c) * p.Cin.ld];
-            D[r + int64_t(c) * p.D.ld] = v;
+            if (Cin) v += beta * __ldcg(Cin + r + int64_t(c) * p.Cin.ld);
+            __stcg(D + r + int64_t(c) * p.D.ld, v);
           }
         }
       }

@@ -7,7 +7,8 @@ import sys
 
 path = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+extra = sys.argv[3:] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", path, *extra, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 fname = ""
 data = []
