@@ -58,6 +58,38 @@ struct Prof {
 };
 static thread_local Prof g_prof;
 
+// ---- library-owned streams for the lookahead schedule (per device, per host thread) ----
+struct LaStreams {
+  cudaStream_t chain = nullptr;  // high priority: panel solve, diagonal block, next-panel updates
+  cudaStream_t bulk = nullptr;   // trailing updates of the rest of the left panel
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  cudaEvent_t ev() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+};
+static thread_local LaStreams g_la[64];
+static bool g_no_lookahead = getenv("CD_NO_LOOKAHEAD") != nullptr;
+
+static LaStreams* la_streams() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  LaStreams& s = g_la[dev];
+  if (!s.chain) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&s.chain, cudaStreamNonBlocking, hi) != cudaSuccess) return nullptr;
+    if (cudaStreamCreateWithPriority(&s.bulk, cudaStreamNonBlocking, lo) != cudaSuccess) return nullptr;
+  }
+  s.next = 0;
+  return &s;
+}
+
 static int note_cuda(cudaError_t e) {
   if (e == cudaSuccess) return CD_SUCCESS;
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
@@ -180,7 +212,7 @@ struct Gemm {
     return *this;
   }
   // D = alpha * sum + beta * Cin
-  void run(Opnd Cin, Opnd D, double alpha, double beta, bool tril, T* part_ws) {
+  void run(Opnd Cin, Opnd D, double alpha, double beta, int tril, T* part_ws) {
     if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
     if (p.nseg == 0) {  // nothing to accumulate: D = beta * Cin
       if (beta == 1.0 && Cin.base == D.base && Cin.arr == D.arr && Cin.off == D.off) return;
@@ -194,7 +226,7 @@ struct Gemm {
     p.D = D;
     p.alpha = alpha;
     p.beta = beta;
-    p.tril = tril ? 1 : 0;
+    p.tril = tril;  // 0 none; 1 + offset (see GemmParams)
     const int64_t tiles = int64_t((p.M + G_BM - 1) / G_BM) * ((p.N + G_BN - 1) / G_BN) * p.batch;
     int splits = 1;
     if (tiles < c.sms && p.KT >= 4) {
@@ -401,7 +433,7 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
       Gemm<T>(c, p, w, 0, 0, batch)
           .seg(Cbar, Dinv_q, w)
           .flops(double(p) * w * (w + 1))  // TRSM  Cbar D^{-1}
-          .run(null_opnd(), W, 1.0, 0.0, false, part_ws);
+          .run(null_opnd(), W, 1.0, 0.0, 0, part_ws);
       if (!w_inplace) run_copy<T>(c, p, w, batch, W, Cbar);
       // Bbar <- Bbar - Cbar R
       if (q > 0)
@@ -411,7 +443,7 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
       Gemm<T>(c, w, w, 1, 0, batch)
           .seg(W, sub(L, k, j), p)
           .flops(double(w) * (w + 1) * p)  // lower triangle only
-          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, true, part_ws);
+          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
     }
     // Dbar <- chol_unblocked_rev(D, Dbar)  (+ S = Dbar + Dbar^T)      (w <= CTA_NMAX)
     run_sweep_small<T>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, q > 0 ? S : null_opnd(), nullptr);
@@ -420,10 +452,96 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
       Gemm<T> g(c, w, q, 1, 0, batch);
       g.seg(S, sub(L, j, 0), w);
       if (p > 0) g.seg(W, sub(L, k, 0), p);
-      g.run(sub(A, j, 0), sub(A, j, 0), -1.0, 1.0, false, part_ws);
+      g.run(sub(A, j, 0), sub(A, j, 0), -1.0, 1.0, 0, part_ws);
     }
   }
   if (info && !c.plan && c.ok()) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_diag_info<T><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
+    c.launched();
+  }
+}
+
+// ------------------------------------------------------------------ blocked reverse, lookahead
+// Same arithmetic as blocked_rev ("the partitioning into columns is
+// arbitrary", 704-707), scheduled on two streams.  For block K = [j, k) with next block
+// K' = [j', j):
+//   chain (high priority):  Cbar <- Cbar D^{-1};
+//        Abar[j:k, j':k] -= W^T L[k:n, j':k]      (Dbar correction + the next panel's
+//                                                  share of Rbar -= Cbar^T B; tril on K)
+//        Dbar <- chol_unblocked_rev(D, Dbar)  (+ S);
+//        [after bulk(K_prev)]  Abar[k:n, j':j] -= W L[j:k, j':j];  Abar[j:k, j':j] -= S L[j:k, j':j]
+//   bulk (low priority):    Abar[k:n, 0:j'] -= W L[j:k, 0:j'];
+//        Abar[j:k, 0:j'] -= [S; W]^T [L[j:k, 0:j']; L[k:n, 0:j']]
+// so the next block's panel solve, correction and diagonal sweep overlap the bulk
+// updates of the current block.  S is double-buffered; each stream has its own split-K
+// partial buffer.
+template <typename T>
+static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info,
+                           T* partA, T* partB) {
+  const int nblk = nblocks(n, nb);
+  T* Dinv = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nblk * nb * nb));
+  T* Sws = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nb * nb * 2));
+  if (c.plan) return;
+  const cudaStream_t caller = c.st;
+  cudaEvent_t e0 = ls->ev();
+  cudaEventRecord(e0, caller);
+  cudaStreamWaitEvent(ls->chain, e0, 0);
+  cudaStreamWaitEvent(ls->bulk, e0, 0);
+  c.st = ls->chain;
+  run_trinv<T>(c, n, nb, true, batch, L, Dinv);
+  cudaEvent_t ev_bulk_prev = nullptr;
+  for (int qb = nblk - 1; qb >= 0 && c.ok(); --qb) {
+    int j, w;
+    block_range(n, nb, true, qb, j, w);
+    const int k = j + w, p = n - k, q = j;
+    int jn = 0, wn = 0;  // next block [jn, j)
+    if (qb > 0) block_range(n, nb, true, qb - 1, jn, wn);
+    const Opnd Dinv_q = ws_opnd(Dinv + int64_t(qb) * nb * nb, int64_t(nblk) * nb * nb, nb);
+    const Opnd S = ws_opnd(Sws + int64_t(qb & 1) * batch * nb * nb, int64_t(nb) * nb, w);
+    const Opnd W = sub(A, k, j);  // Cbar, solved in place
+    c.st = ls->chain;
+    if (p > 0) {
+      Gemm<T>(c, p, w, 0, 0, batch)
+          .seg(W, Dinv_q, w)
+          .flops(double(p) * w * (w + 1))  // TRSM  Cbar D^{-1}
+          .run(null_opnd(), W, 1.0, 0.0, 0, partA);
+      // Dbar -= tril(Cbar^T C)  and  Rbar[:, jn:j] -= Cbar^T B[:, jn:j]
+      Gemm<T>(c, w, wn + w, 1, 0, batch)
+          .seg(W, sub(L, k, jn), p)
+          .flops(double(w) * (w + 1) * p + 2.0 * w * wn * p)
+          .run(sub(A, j, jn), sub(A, j, jn), -1.0, 1.0, 1 + wn, partA);
+    }
+    run_sweep_small<T>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, q > 0 ? S : null_opnd(), nullptr);
+    if (q == 0) break;
+    cudaEvent_t ev_s = ls->ev();
+    cudaEventRecord(ev_s, ls->chain);
+    if (ev_bulk_prev) cudaStreamWaitEvent(ls->chain, ev_bulk_prev, 0);
+    // next panel [jn, j):  Bbar part (rows k..n) and the S R part of Rbar (rows j..k)
+    if (p > 0)
+      Gemm<T>(c, p, wn, 0, 0, batch).seg(W, sub(L, j, jn), w).run(sub(A, k, jn), sub(A, k, jn), -1.0, 1.0, 0, partA);
+    Gemm<T>(c, w, wn, 1, 0, batch).seg(S, sub(L, j, jn), w).run(sub(A, j, jn), sub(A, j, jn), -1.0, 1.0, 0, partA);
+    if (jn > 0) {
+      c.st = ls->bulk;
+      cudaStreamWaitEvent(ls->bulk, ev_s, 0);
+      if (p > 0)
+        Gemm<T>(c, p, jn, 0, 0, batch).seg(W, sub(L, j, 0), w).run(sub(A, k, 0), sub(A, k, 0), -1.0, 1.0, 0, partB);
+      Gemm<T> g(c, w, jn, 1, 0, batch);
+      g.seg(S, sub(L, j, 0), w);
+      if (p > 0) g.seg(W, sub(L, k, 0), p);
+      g.run(sub(A, j, 0), sub(A, j, 0), -1.0, 1.0, 0, partB);
+      ev_bulk_prev = ls->ev();
+      cudaEventRecord(ev_bulk_prev, ls->bulk);
+    }
+  }
+  // join both streams back into the caller's stream
+  cudaEvent_t e1 = ls->ev(), e2 = ls->ev();
+  cudaEventRecord(e1, ls->chain);
+  cudaEventRecord(e2, ls->bulk);
+  cudaStreamWaitEvent(caller, e1, 0);
+  cudaStreamWaitEvent(caller, e2, 0);
+  c.st = caller;
+  if (info && c.ok()) {
     c.pre(CD_PROF_OTHER, 0.0);
     k_diag_info<T><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
     c.launched();
@@ -458,17 +576,17 @@ static void blocked_fwd(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
           .seg(sub(A, j, 0), sub(L, j, 0), q)
           .seg(sub(L, j, 0), sub(A, j, 0), q)
           .flops(2.0 * w * (w + 1) * q)  // lower triangle only
-          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, true, part_ws);
+          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
     run_sweep_small<T>(c, false, w, batch, sub(L, j, j), sub(A, j, j), 0, p > 0 ? Dc : null_opnd(), nullptr);
     if (p > 0) {
       Gemm<T> g(c, p, w, 0, 1, batch);
       if (q > 0) g.seg(sub(A, k, 0), sub(L, j, 0), q).seg(sub(L, k, 0), sub(A, j, 0), q);
       g.seg(sub(L, k, j), Dc, w);
-      g.run(sub(A, k, j), W, -1.0, 1.0, false, part_ws);
+      g.run(sub(A, k, j), W, -1.0, 1.0, 0, part_ws);
       Gemm<T>(c, p, w, 0, 1, batch)
           .seg(W, Dinv_q, w)
           .flops(double(p) * w * (w + 1))  // TRSM  X D^{-T}
-          .run(null_opnd(), sub(A, k, j), 1.0, 0.0, false, part_ws);
+          .run(null_opnd(), sub(A, k, j), 1.0, 0.0, 0, part_ws);
     }
   }
   if (info && !c.plan && c.ok()) {
@@ -508,8 +626,15 @@ static void drive(Ctx& c, const Call& k) {
     return;
   }
   T* part = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
-  if (k.op == CD_OP_REV) blocked_rev<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
-  else blocked_fwd<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+  if (k.op == CD_OP_REV) {
+    // lookahead schedule needs a one-tile-wide block (in-place panel solve) and library streams
+    T* part2 = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
+    LaStreams* ls = (!g_no_lookahead && nb <= G_BN) ? (c.plan ? reinterpret_cast<LaStreams*>(1) : la_streams()) : nullptr;
+    if (ls) blocked_rev_la<T>(c, ls, n, nb, k.batch, k.L, k.A, k.info, part, part2);
+    else blocked_rev<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+  } else {
+    blocked_fwd<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+  }
   if (k.op == CD_OP_REV && k.o.out_mode != CD_OUT_TRIL && !c.plan && c.ok()) {
     c.pre(CD_PROF_OTHER, 0.0);
     k_out_mode<T><<<grid_1d(int64_t(n) * n * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, k.A, k.o.out_mode);

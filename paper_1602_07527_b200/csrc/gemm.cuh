@@ -37,7 +37,7 @@ struct GemmParams {
   Opnd Cin;  // beta * Cin (ignored if beta == 0)
   Opnd D;    // output
   double alpha, beta;
-  int tril;   // write only rows >= cols (view coordinates)
+  int tril;   // 0: full output; t > 0: write only rows r, cols c with r + (t - 1) >= c
   void* part; // split-K partials: [split][batch][N][M]
 };
 
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(GemmParams p) {
         for (int e = 0; e < 2; ++e) {
           const int r = m0 + wm * 64 + i * 8 + g;
           const int c = n0 + wn * 32 + j * 8 + 2 * t + e;
-          if (r < p.M && c < p.N && (!p.tril || r >= c)) {
+          if (r < p.M && c < p.N && (!p.tril || r + p.tril - 1 >= c)) {
             if (part) {
               part[r + int64_t(c) * p.M] = acc[i][j][e];
             } else {
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(GemmParams p) {
       for (int i = 0; i < 8; ++i) {
         const int r = m0 + (i < 4 ? tr * 4 + i : 64 + tr * 4 + i - 4);
         const int c = n0 + (j < 4 ? tc * 4 + j : 64 + tc * 4 + j - 4);
-        if (r < p.M && c < p.N && (!p.tril || r >= c)) {
+        if (r < p.M && c < p.N && (!p.tril || r + p.tril - 1 >= c)) {
           if (part) {
             part[r + int64_t(c) * p.M] = acc[i][j];
           } else {
@@ -266,18 +266,30 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(GemmParams p) {
 }
 
 // Deterministic split-K reduction: D = alpha * sum_{s=0..S-1} part[s] + beta * Cin.
+// The fixed summation order ((s0 + s1) + (s2 + s3)) + ... keeps results bitwise
+// reproducible; four independent partial sums keep the loads in flight.
 template <typename T>
 __global__ void k_splitk_reduce(int M, int N, int64_t batch, int splits, const T* __restrict__ part, Opnd Cin,
                                 Opnd D, double alpha, double beta, int tril) {
   const int64_t MN = int64_t(M) * N, total = MN * batch;
+  const int64_t sstride = MN * batch;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
     const int r = int(idx % M);
     const int c = int((idx / M) % N);
     const int64_t b = idx / MN;
-    if (tril && r < c) continue;
-    T s = T(0);
-    for (int q = 0; q < splits; ++q) s += part[(int64_t(q) * batch + b) * MN + r + int64_t(c) * M];
+    if (tril && r + tril - 1 < c) continue;
+    const T* pp = part + b * MN + r + int64_t(c) * M;
+    T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+    int q = 0;
+    for (; q + 4 <= splits; q += 4) {
+      s0 += __ldcg(pp + int64_t(q) * sstride);
+      s1 += __ldcg(pp + int64_t(q + 1) * sstride);
+      s2 += __ldcg(pp + int64_t(q + 2) * sstride);
+      s3 += __ldcg(pp + int64_t(q + 3) * sstride);
+    }
+    for (; q < splits; ++q) s0 += __ldcg(pp + int64_t(q) * sstride);
+    const T s = (s0 + s1) + (s2 + s3);
     T v = T(alpha) * s;
     if (beta != 0.0) v += T(beta) * optr<T>(Cin, b)[r + int64_t(c) * Cin.ld];
     optr_w<T>(D, b)[r + int64_t(c) * D.ld] = v;

@@ -90,9 +90,9 @@ template <int TA, int TB>
 __global__ void __launch_bounds__(TG_THREADS, 1) k_gemm_tma(const GemmParams p, const __grid_constant__ TmaMaps tm) {
   using Lay = TmaLayout<TA, TB>;
   constexpr int BM = Lay::BM, BN = Lay::BN, BK = Lay::BK;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_tma[];
   // 1024-byte aligned carve-up: [A stages][B stages][full bars][empty bars]
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_tma) + 1023) & ~uintptr_t(1023));
   double* As = reinterpret_cast<double*>(base);
   double* Bs = As + TG_STAGES * Lay::A_SIZE;
   uint64_t* full = reinterpret_cast<uint64_t*>(Bs + TG_STAGES * Lay::B_SIZE);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1) k_gemm_tma(const GemmParams p, 
       for (int e = 0; e < 2; ++e) {
         const int r = m0 + wm * 64 + i * 8 + g;
         const int c = n0 + wn * 32 + j * 8 + 2 * t + e;
-        if (r < p.M && c < p.N && (!p.tril || r >= c)) {
+        if (r < p.M && c < p.N && (!p.tril || r + p.tril - 1 >= c)) {
           if (part) {
             __stcg(part + r + int64_t(c) * p.M, acc[i][j][e]);
           } else if (pre) {
