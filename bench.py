@@ -403,7 +403,7 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
                        f"sharded by matrix over {P} GPU(s)",
            "value": round(mats, 1), "unit": "matrices/s", "ms_per_step": round(worst, 4),
            "gflops": round(mats * rev_flops(n) / 1e9, 1), "steps": args.steps_batched,
-           "roofline": {"kernel": "k_sweep_warp_rev<double>", "bound": "hbm", "achieved": round(achieved_gbs, 1),
+           "roofline": {"kernel": "k_rev_dmma32<4> (one warp per matrix, N_b=8 DMMA tiles)", "bound": "hbm", "achieved": round(achieved_gbs, 1),
                         "peak": hbm, "unit": "GB/s", "frac": round(achieved_gbs / hbm, 4),
                         "algorithmic_bytes_per_matrix": algo_bytes,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs", "traffic": load_traffic("batched32")},
@@ -444,6 +444,66 @@ def cpu_sample_batched(L, Lb, n, sample=16384):
     return {"value": round(s / dt, 1), "unit": "matrices/s", "cores": ncores,
             "threads": int(os.environ.get("OMP_NUM_THREADS", ncores)), "kind": "oracle",
             "sample": f"first {s} of the 65536 N={n} matrices, oracle/oracle.c or_chol_rev_batched (OpenMP over matrices)"}
+
+
+def bench_small_configs(args, dist: Dist):
+    """configs[0] (N=64 rev latency), configs[1] (N=1024 rev + fwd) and configs[3]
+    (1024 x N=512 fp32 rev + fwd, sharded by matrix), same timing rules."""
+    import torch
+    import paper_1602_07527_b200 as cd
+    import synthetic
+
+    dev = dist.device
+    stream = torch.cuda.current_stream(dev)
+    out = {}
+    # configs[0]: single fp64 N=64 reverse (latency)
+    L, Lb, _ = synthetic.draw(64, 0)
+    Ld, A0 = colmajor_dev(L, dev), colmajor_dev(Lb, dev)
+    A = A0.clone()
+    ms = timed_steps(lambda: cd.chol_rev(Ld, A), lambda: A.copy_(A0), 50, args.warmup, dist, stream)
+    t = dist.max(statistics.median(ms))
+    out["n64_rev"] = {"workload": "configs[0]: chol_rev fp64 N=64, seed 0", "us_per_call": round(t * 1e3, 2),
+                      "gflops": round(rev_flops(64) / (t * 1e-3) / 1e9, 2)}
+    # configs[1]: N=1024 reverse and forward
+    L, Lb, Sd = synthetic.draw(1024, 0, sdot=True)
+    Ld, A0, F0 = colmajor_dev(L, dev), colmajor_dev(Lb, dev), colmajor_dev(np.tril(Sd), dev)
+    A, F = A0.clone(), F0.clone()
+    tr = dist.max(statistics.median(timed_steps(lambda: cd.chol_rev(Ld, A), lambda: A.copy_(A0), 10, args.warmup,
+                                                dist, stream)))
+    tf = dist.max(statistics.median(timed_steps(lambda: cd.chol_fwd(Ld, F), lambda: F.copy_(F0), 10, args.warmup,
+                                                dist, stream)))
+    out["n1024"] = {"workload": "configs[1]: fp64 N=1024, seed 0", "rev_ms": round(tr, 3), "fwd_ms": round(tf, 3),
+                    "rev_gflops": round(rev_flops(1024) / (tr * 1e-3) / 1e9, 1),
+                    "fwd_gflops": round(fwd_flops(1024) / (tf * 1e-3) / 1e9, 1)}
+    # configs[3]: 1024 x N=512 fp32, reverse + forward per step, sharded by matrix
+    n, total = 512, 1024
+    P, r = dist.world, dist.rank
+    lo, hi = r * total // P, (r + 1) * total // P
+    L, Lb, Sd = synthetic.draw_batch(n, hi - lo, seed=0, sdot=True, start=lo)
+    Ld = colmajor_dev(L, dev, torch.float32)
+    A0 = colmajor_dev(Lb, dev, torch.float32)
+    F0 = colmajor_dev(np.tril(Sd), dev, torch.float32)
+    del L, Lb, Sd
+    A, F = A0.clone(), F0.clone()
+
+    def step():
+        cd.chol_rev(Ld, A)
+        cd.chol_fwd(Ld, F)
+
+    def restore():
+        A.copy_(A0)
+        F.copy_(F0)
+
+    t = dist.max(statistics.median(timed_steps(step, restore, 5, args.warmup, dist, stream)))
+    fl = (rev_flops(n) + fwd_flops(n)) * total
+    out["batched_f32_n512"] = {
+        "workload": f"configs[3]: fp32 rev + fwd, {total} x N={n}, sharded by matrix over {P} GPU(s)",
+        "ms_per_step": round(t, 3), "matrices_per_s": round(total / (t * 1e-3), 1),
+        "gflops": round(fl / (t * 1e-3) / 1e9, 1),
+        "roofline": {"bound": "fp32 SIMT (FFMA) in round 1", "peak_tflops": 74.4,
+                     "frac": round(fl / (t * 1e-3) / 1e12 / 74.4, 4),
+                     "peak_source": "nominal 148 SM x 128 FFMA/clk x 2 x 1.965 GHz (cuBLAS SGEMM measured 64.0)"}}
+    return out
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -509,6 +569,7 @@ def main():
     ap.add_argument("--ref-cols", type=int, default=1024)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batched", action="store_true")
+    ap.add_argument("--no-aux", action="store_true", help="skip configs[0], [1], [3] sub-measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -530,6 +591,8 @@ def main():
     res = bench_single_rev(args, dist)
     if not args.no_batched:
         res["batched"] = bench_batched(args, dist)
+    if not args.no_aux:
+        res["other_configs"] = bench_small_configs(args, dist)
     if dist.rank == 0:
         print(json.dumps(res), flush=True)
     dist.close()

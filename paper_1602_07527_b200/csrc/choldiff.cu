@@ -30,6 +30,7 @@
 #include "sweep_cta.cuh"
 #include "sweep_warp.cuh"
 #include "sweep_dmma32.cuh"
+#include "sweep_dmma_cta.cuh"
 
 namespace cd {
 
@@ -361,6 +362,28 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
       k_sym2<T><<<grid_1d(total, 256, c.sms), 256, 0, c.st>>>(n, batch, A, S, rev ? 0 : 1);
       c.launched();
     }
+  } else if (rev && sizeof(T) == 8) {
+    // fp64 reverse, 32 < n <= 128: N_b = 8 blocked sweep on DMMA tiles, one CTA per matrix
+    const int nblk = (n + 7) / 8;
+    auto go = [&](auto kern, size_t smem) {
+      set_smem(kern, smem);
+      kern<<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+    };
+    switch (nblk) {
+      case 5: go(k_rev_dmma_cta<5>, dmma_cta_smem<5>()); break;
+      case 6: go(k_rev_dmma_cta<6>, dmma_cta_smem<6>()); break;
+      case 7: go(k_rev_dmma_cta<7>, dmma_cta_smem<7>()); break;
+      case 8: go(k_rev_dmma_cta<8>, dmma_cta_smem<8>()); break;
+      case 9: go(k_rev_dmma_cta<9>, dmma_cta_smem<9>()); break;
+      case 10: go(k_rev_dmma_cta<10>, dmma_cta_smem<10>()); break;
+      case 11: go(k_rev_dmma_cta<11>, dmma_cta_smem<11>()); break;
+      case 12: go(k_rev_dmma_cta<12>, dmma_cta_smem<12>()); break;
+      case 13: go(k_rev_dmma_cta<13>, dmma_cta_smem<13>()); break;
+      case 14: go(k_rev_dmma_cta<14>, dmma_cta_smem<14>()); break;
+      case 15: go(k_rev_dmma_cta<15>, dmma_cta_smem<15>()); break;
+      default: go(k_rev_dmma_cta<16>, dmma_cta_smem<16>()); break;
+    }
+    c.launched();
   } else {
     const size_t smem = sweep_cta_smem<T>(n);
     if (rev) {
