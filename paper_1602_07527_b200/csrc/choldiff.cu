@@ -30,6 +30,7 @@
 #include "sweep_cta.cuh"
 #include "sweep_warp.cuh"
 #include "sweep_dmma32.cuh"
+#include "sweep_reg32.cuh"
 #include "sweep_dmma_cta.cuh"
 
 namespace cd {
@@ -76,6 +77,7 @@ struct LaStreams {
 };
 static thread_local LaStreams g_la[64];
 static bool g_no_lookahead = getenv("CD_NO_LOOKAHEAD") != nullptr;
+static bool g_reg32 = getenv("CD_SMEM32") == nullptr;  // register-resident small-n kernel (default)
 
 static LaStreams* la_streams() {
   int dev = 0;
@@ -344,7 +346,19 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
         kern<<<g2, D32_WPB * 32, sm2, c.st>>>(n, batch, Lo, Ao, out_mode, info);
       };
       const int nblk = (n + 7) / 8;
-      if (nblk == 1) go(k_rev_dmma32<1>);
+      if (g_reg32) {
+        // register-resident variant (sweep_reg32.cuh)
+        const size_t sm3 = reg32_smem();
+        const unsigned g3 = unsigned(std::min<int64_t>((batch + R32_WPB - 1) / R32_WPB, int64_t(c.sms) * 16));
+        auto go3 = [&](auto kern) {
+          set_smem(kern, sm3);
+          kern<<<g3, R32_WPB * 32, sm3, c.st>>>(n, batch, Lo, Ao, out_mode, info);
+        };
+        if (nblk == 1) go3(k_rev_reg32<1>);
+        else if (nblk == 2) go3(k_rev_reg32<2>);
+        else if (nblk == 3) go3(k_rev_reg32<3>);
+        else go3(k_rev_reg32<4>);
+      } else if (nblk == 1) go(k_rev_dmma32<1>);
       else if (nblk == 2) go(k_rev_dmma32<2>);
       else if (nblk == 3) go(k_rev_dmma32<3>);
       else go(k_rev_dmma32<4>);
