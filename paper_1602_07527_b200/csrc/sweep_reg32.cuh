@@ -54,7 +54,7 @@ __device__ __forceinline__ void r32_transpose(double c0, double c1, int g, int t
 }
 
 template <int NBLK>
-__global__ void __launch_bounds__(R32_WPB * 32)
+__global__ void __launch_bounds__(R32_WPB * 32, 3)
     k_rev_reg32(int n, int64_t batch, Opnd Ld, Opnd Ad, int out_mode, int* __restrict__ info) {
   constexpr int NT = NBLK * (NBLK + 1) / 2;  // lower tiles
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -70,28 +70,47 @@ __global__ void __launch_bounds__(R32_WPB * 32)
     double* Ag = optr_w<double>(Ad, b);
     double Lt[NT][2], Ac[NT][2];
     // ---- loads (lower triangles only; padding -> blockdiag(I) / 0)
+    if (n == 8 * NBLK) {  // no padding: only the diagonal tiles are masked
 #pragma unroll
-    for (int bj = 0; bj < NBLK; ++bj)
+      for (int bj = 0; bj < NBLK; ++bj)
 #pragma unroll
-      for (int bi = bj; bi < NBLK; ++bi) {
-        const int ti = TI(bi, bj);
+        for (int bi = bj; bi < NBLK; ++bi) {
+          const int ti = TI(bi, bj);
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const int r = 8 * bi + 4 * kk + t, c = 8 * bj + g;
-          double v = 0.0;
-          if (r < n && c < n) {
-            if (r >= c) v = Lg[r + int64_t(c) * Ld.ld];
-          } else if (r == c) {
-            v = 1.0;
+          for (int kk = 0; kk < 2; ++kk) {
+            const int r = 8 * bi + 4 * kk + t, c = 8 * bj + g;
+            Lt[ti][kk] = (bi > bj || r >= c) ? __ldg(Lg + r + int64_t(c) * Ld.ld) : 0.0;
           }
-          Lt[ti][kk] = v;
-        }
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
-          Ac[ti][e] = (r < n && c < n && r >= c) ? Ag[r + int64_t(c) * Ad.ld] : 0.0;
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
+            Ac[ti][e] = (bi > bj || r >= c) ? Ag[r + int64_t(c) * Ad.ld] : 0.0;
+          }
         }
-      }
+    } else {
+#pragma unroll
+      for (int bj = 0; bj < NBLK; ++bj)
+#pragma unroll
+        for (int bi = bj; bi < NBLK; ++bi) {
+          const int ti = TI(bi, bj);
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int r = 8 * bi + 4 * kk + t, c = 8 * bj + g;
+            double v = 0.0;
+            if (r < n && c < n) {
+              if (r >= c) v = Lg[r + int64_t(c) * Ld.ld];
+            } else if (r == c) {
+              v = 1.0;
+            }
+            Lt[ti][kk] = v;
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
+            Ac[ti][e] = (r < n && c < n && r >= c) ? Ag[r + int64_t(c) * Ad.ld] : 0.0;
+          }
+        }
+    }
     // ---- diagonal blocks of L -> smem (for their inverses), info
     __syncwarp();
 #pragma unroll
@@ -102,12 +121,15 @@ __global__ void __launch_bounds__(R32_WPB * 32)
     {
       const int blk = lane >> 3, c = lane & 7;
       bool bad = false;
-      if (blk < NBLK) {
-        const double* D = sD + blk * 64;
-        bad = (8 * blk + c < n) && bad_pivot(D[c * 8 + c]);
+      {  // all lanes take part (shuffles); lanes of blocks >= NBLK work on tile 0 and discard
+        const double* D = sD + (blk < NBLK ? blk : 0) * 64;
+        bad = blk < NBLK && (8 * blk + c < n) && bad_pivot(D[c * 8 + c]);
+        // 1/D(r,r), r = 0..7: each lane computes its own column's, the rest by shuffle
+        const double rdc = 1.0 / D[c * 8 + c];
         double x[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
+          const double rdr = __shfl_sync(0xffffffffu, rdc, (lane & ~7) | r);
           if (r < c) {
             x[r] = 0.0;
           } else {
@@ -115,11 +137,13 @@ __global__ void __launch_bounds__(R32_WPB * 32)
 #pragma unroll
             for (int q = 0; q < r; ++q)
               if (q >= c) s -= D[q * 8 + r] * x[q];
-            x[r] = s / D[r * 8 + r];
+            x[r] = s * rdr;
           }
         }
+        if (blk < NBLK) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) sDi[blk * 64 + c * 8 + r] = x[r];  // Dinv(r, c), col-major
+          for (int r = 0; r < 8; ++r) sDi[blk * 64 + c * 8 + r] = x[r];  // Dinv(r, c), col-major
+        }
       }
       const unsigned msk = __ballot_sync(0xffffffffu, bad);
       if (info && lane == 0) {
@@ -232,20 +256,32 @@ __global__ void __launch_bounds__(R32_WPB * 32)
     }
 
     // ---- store tril(Sigma_bar) (and the requested mirror)
+    if (out_mode == 0 && n == 8 * NBLK) {
 #pragma unroll
-    for (int bj = 0; bj < NBLK; ++bj)
+      for (int bj = 0; bj < NBLK; ++bj)
 #pragma unroll
-      for (int bi = bj; bi < NBLK; ++bi)
+        for (int bi = bj; bi < NBLK; ++bi)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
-          if (r < n && c < n && r >= c) {
-            double v = Ac[TI(bi, bj)][e];
-            if (out_mode == 2 && r != c) v *= 0.5;
-            Ag[r + int64_t(c) * Ad.ld] = v;
-            if (out_mode != 0 && r != c) Ag[c + int64_t(r) * Ad.ld] = v;
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
+            if (bi > bj || r >= c) Ag[r + int64_t(c) * Ad.ld] = Ac[TI(bi, bj)][e];
           }
-        }
+    } else {
+#pragma unroll
+      for (int bj = 0; bj < NBLK; ++bj)
+#pragma unroll
+        for (int bi = bj; bi < NBLK; ++bi)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
+            if (r < n && c < n && r >= c) {
+              double v = Ac[TI(bi, bj)][e];
+              if (out_mode == 2 && r != c) v *= 0.5;
+              Ag[r + int64_t(c) * Ad.ld] = v;
+              if (out_mode != 0 && r != c) Ag[c + int64_t(r) * Ad.ld] = v;
+            }
+          }
+    }
   }
 }
 
