@@ -373,8 +373,9 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
     import paper_1602_07527_b200 as cd
     import synthetic
 
+    from paper_1602_07527_b200.shard import gather_batches, shard_range
     P, r = dist.world, dist.rank
-    lo, hi = r * total // P, (r + 1) * total // P
+    lo, hi = shard_range(total, P, r)
     B = hi - lo
     L, Lb, _ = synthetic.draw_batch(n, B, seed=seed, start=lo)
     dev = dist.device
@@ -410,21 +411,19 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
            "gpu_launches": int(launches), "clocks": clk.summary()}
     if gather and P > 1:
         # NCCL used only to gather the sharded results (north star), timed separately
-        import torch.distributed as tdist
-        outbuf = torch.empty((total, n, n), dtype=torch.float64, device=dev)
-        src = A.transpose(-1, -2).contiguous()
         torch.cuda.synchronize()
         dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        if total % P == 0:
-            tdist.all_gather_into_tensor(outbuf, src)
+        gathered = gather_batches(A, total)
         b.record(stream)
         torch.cuda.synchronize()
         g = dist.max(a.elapsed_time(b))
+        del gathered
         out["gather"] = {"ms": round(g, 3), "bytes": total * n * n * 8,
-                         "GBps": round(total * n * n * 8 / (g * 1e-3) / 1e9, 1), "collective": "all_gather_into_tensor"}
+                         "GBps": round(total * n * n * 8 / (g * 1e-3) / 1e9, 1),
+                         "collective": "all_gather_into_tensor (paper_1602_07527_b200/shard.py)"}
     if dist.world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_sample_batched(L, Lb, n)
     return out
@@ -477,8 +476,9 @@ def bench_small_configs(args, dist: Dist):
                     "fwd_gflops": round(fwd_flops(1024) / (tf * 1e-3) / 1e9, 1)}
     # configs[3]: 1024 x N=512 fp32, reverse + forward per step, sharded by matrix
     n, total = 512, 1024
+    from paper_1602_07527_b200.shard import shard_range
     P, r = dist.world, dist.rank
-    lo, hi = r * total // P, (r + 1) * total // P
+    lo, hi = shard_range(total, P, r)
     L, Lb, Sd = synthetic.draw_batch(n, hi - lo, seed=0, sdot=True, start=lo)
     Ld = colmajor_dev(L, dev, torch.float32)
     A0 = colmajor_dev(Lb, dev, torch.float32)

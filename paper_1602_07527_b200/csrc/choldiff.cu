@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "gemm_tma.cuh"
+#include "gemm_tc32.cuh"
 #include "misc.cuh"
 #include "sweep_cta.cuh"
 #include "sweep_warp.cuh"
@@ -182,6 +183,25 @@ static bool make_tmap(CUtensorMap* map, int* shift, const void* p, int64_t rows,
   return r == CUDA_SUCCESS;
 }
 
+// fp32 map with 128-byte swizzle for the tcgen05 kernel (gemm_tc32.cuh)
+static bool make_tmap_f32_sw128(CUtensorMap* map, const void* p, int64_t rows, int64_t cols, int64_t ld,
+                                int64_t bstride, int64_t batch, int box0, int box1) {
+  auto enc = tmap_encoder();
+  if (!enc || rows <= 0 || cols <= 0) return false;
+  if (reinterpret_cast<uintptr_t>(p) % 16) return false;
+  if ((ld * 4) % 16 || (batch > 1 && (bstride * 4) % 16)) return false;
+  cuuint64_t dims[3] = {cuuint64_t(rows), cuuint64_t(cols), cuuint64_t(std::max<int64_t>(batch, 1))};
+  cuuint64_t strides[2] = {cuuint64_t(ld * 4), cuuint64_t(std::max<int64_t>(bstride, 1) * 4)};
+  cuuint32_t box[3] = {cuuint32_t(box0), cuuint32_t(box1), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const cuuint32_t rank = batch > 1 ? 3 : 2;
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
+
 // ------------------------------------------------------------------ GEMM launcher
 constexpr int64_t PART_TILES = 2 * 152;  // split-K partial budget, in 128x128 output tiles
 
@@ -297,7 +317,39 @@ struct Gemm {
     c.launched();
     return true;
   }
+  // fp32: tcgen05 kind::tf32 kernel when every operand can be described by a TMA map
+  template <int A_, int B_>
+  bool launch_tc32(dim3 grid) {
+    if (g_tc32_disabled) return false;
+    TmaMaps tm;
+    memset(&tm, 0, sizeof(tm));
+    tm.batched = p.batch > 1 ? 1 : 0;
+    for (int s = 0; s < p.nseg; ++s) {
+      const GemmSeg& sg = p.seg[s];
+      if (sg.A.arr || sg.B.arr) return false;
+      const T* pa = static_cast<const T*>(sg.A.base) + sg.A.off;
+      const T* pb = static_cast<const T*>(sg.B.base) + sg.B.off;
+      const bool okA = A_ == 0 ? make_tmap_f32_sw128(&tm.a[s], pa, p.M, sg.K, sg.A.ld, sg.A.stride, p.batch, 32, 32)
+                               : make_tmap_f32_sw128(&tm.a[s], pa, sg.K, p.M, sg.A.ld, sg.A.stride, p.batch, 32, 128);
+      const bool okB = B_ == 0 ? make_tmap_f32_sw128(&tm.b[s], pb, sg.K, p.N, sg.B.ld, sg.B.stride, p.batch, 32, 128)
+                               : make_tmap_f32_sw128(&tm.b[s], pb, p.N, sg.K, sg.B.ld, sg.B.stride, p.batch, 32, 32);
+      if (!okA || !okB) return false;
+    }
+    auto kern = k_gemm_tc32<A_, B_>;
+    set_smem(kern, TC_SMEM);
+    kern<<<grid, TC_THREADS, TC_SMEM, c.st>>>(p, tm);
+    c.launched();
+    return true;
+  }
   void launch(dim3 grid) {
+    if constexpr (sizeof(T) == 4) {
+      bool done = false;
+      if (TA == 0 && TB == 0) done = launch_tc32<0, 0>(grid);
+      else if (TA == 0 && TB == 1) done = launch_tc32<0, 1>(grid);
+      else if (TA == 1 && TB == 0) done = launch_tc32<1, 0>(grid);
+      else done = launch_tc32<1, 1>(grid);
+      if (done) return;
+    }
     if constexpr (sizeof(T) == 8) {
       bool done = false;
       if (TA == 0 && TB == 0) done = launch_tma<0, 0>(grid);

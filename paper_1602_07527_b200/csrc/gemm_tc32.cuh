@@ -1,0 +1,214 @@
+// gemm_tc32.cuh -- fp32 Level-3 updates of the blocked sweeps (PAPER.md:634-636, 655-666,
+// 689-701) on the 5th-generation tensor cores: tcgen05.mma kind::tf32 with the
+// accumulator in TMEM, operands staged by TMA (128-byte swizzle) into a 4-stage ring.
+//
+//   warp 0 lane 0 : TMA producer (cp.async.bulk.tensor, mbarrier complete_tx)
+//   warp 1 lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128 N=128 K=8;
+//                   tcgen05.commit releases each smem stage and finally the accumulator)
+//   warps 0..3    : epilogue (tcgen05.ld 32x32b: thread = accumulator row; coalesced
+//                   column-major stores, alpha/beta, tril mask, split-K partials)
+//
+// Operand layouts: K-contiguous operands use the K-major SW128 canonical layout (one
+// TMA box of 32 x 128); M/N-contiguous operands use the MN-major SW128 layout (four TMA
+// boxes of 32 x 32).  TF32 operands (10-bit mantissa, products accumulated in fp32):
+// DESIGN.md §6 gives the error budget against the 1e-4 gate.  Same GemmParams
+// semantics as k_gemm / k_gemm_tma.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "gemm_tma.cuh"  // mbarrier / TMA helpers, TmaMaps
+
+namespace cd {
+
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 128;
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32;
+constexpr uint32_t TC_STAGE_BYTES = (TC_BM + TC_BN) * TC_BK * 4;  // 32 KB
+constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version (Blackwell)
+  d |= uint64_t(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, M=128, N=128, majors per operand
+__host__ __device__ constexpr uint32_t tc_idesc(int a_mn_major, int b_mn_major) {
+  return (1u << 4)                       // c_format = F32
+         | (2u << 7) | (2u << 10)        // a_format = b_format = TF32
+         | (uint32_t(a_mn_major) << 15)  // a_major (1 = MN)
+         | (uint32_t(b_mn_major) << 16)  // b_major
+         | ((128u >> 3) << 17)           // N >> 3
+         | ((128u >> 4) << 24);          // M >> 4
+}
+
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
+  // bounded wait: a protocol error becomes a trap instead of a hung GPU
+  uint32_t spins = 0;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++spins > (1u << 26)) __trap();
+  }
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm) {
+  extern __shared__ __align__(1024) unsigned char smem_tc[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_tc) + 1023) & ~uintptr_t(1023));
+  unsigned char* As = base;                                   // stages of A (16 KB each)
+  unsigned char* Bs = base + TC_STAGES * (TC_BM * TC_BK * 4);  // stages of B (16 KB each)
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + TC_STAGES * TC_STAGE_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* accf = empty + TC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t zb = blockIdx.z;
+  const int split = int(zb % p.splits);
+  const int64_t b = zb / p.splits;
+  const int m0 = blockIdx.x * TC_BM, n0 = blockIdx.y * TC_BN;
+  const int kt0 = split * p.kt_per_split;
+  const int kt1 = min(p.KT, kt0 + p.kt_per_split);
+  const int nkt = kt1 - kt0;
+
+  if (tid == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: 128 columns x 128 lanes of fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    for (int it = 0; it < nkt; ++it) {
+      const int s = it % TC_STAGES;
+      if (it >= TC_STAGES) tc_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
+      const int kt = kt0 + it;
+      int sg = 0;
+      if (p.nseg > 1 && kt * TC_BK >= p.seg[1].kv0) sg = 1;
+      if (p.nseg > 2 && kt * TC_BK >= p.seg[2].kv0) sg = 2;
+      const int kl = kt * TC_BK - p.seg[sg].kv0;
+      mbar_expect_tx(&full[s], TC_STAGE_BYTES);
+      unsigned char* as = As + s * (TC_BM * TC_BK * 4);
+      unsigned char* bs = Bs + s * (TC_BN * TC_BK * 4);
+      if (TA == 0) {  // MN-major: four 32(M) x 32(K) boxes
+        for (int c = 0; c < 4; ++c) {
+          if (tm.batched) tma_load_3d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, int(b), &full[s]);
+          else tma_load_2d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, &full[s]);
+        }
+      } else {  // K-major: one 32(K) x 128(M) box
+        if (tm.batched) tma_load_3d(as, &tm.a[sg], kl, m0, int(b), &full[s]);
+        else tma_load_2d(as, &tm.a[sg], kl, m0, &full[s]);
+      }
+      if (TB == 1) {  // MN-major B
+        for (int c = 0; c < 4; ++c) {
+          if (tm.batched) tma_load_3d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, int(b), &full[s]);
+          else tma_load_2d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, &full[s]);
+        }
+      } else {
+        if (tm.batched) tma_load_3d(bs, &tm.b[sg], kl, n0, int(b), &full[s]);
+        else tma_load_2d(bs, &tm.b[sg], kl, n0, &full[s]);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = tc_idesc(TA == 0 ? 1 : 0, TB == 1 ? 1 : 0);
+    for (int it = 0; it < nkt; ++it) {
+      const int s = it % TC_STAGES;
+      tc_wait(&full[s], (it / TC_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t sa = smem_u32(As + s * (TC_BM * TC_BK * 4));
+      const uint32_t sb = smem_u32(Bs + s * (TC_BN * TC_BK * 4));
+#pragma unroll
+      for (int kk = 0; kk < TC_BK / 8; ++kk) {
+        // K-major: advance 32 B along K inside the swizzle atom; MN-major: next 8-row K group (1 KB)
+        const uint64_t da = (TA == 0) ? umma_desc(sa + kk * 1024, 4096, 1024) : umma_desc(sa + kk * 32, 16, 1024);
+        const uint64_t db = (TB == 1) ? umma_desc(sb + kk * 1024, 4096, 1024) : umma_desc(sb + kk * 32, 16, 1024);
+        const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+        asm volatile(
+            "{\n.reg .pred P;\nsetp.ne.b32 P, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, P;\n}\n" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       smem_u32(&empty[s]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(accf))
+                 : "memory");
+  }
+
+  // ---------------- epilogue: thread = accumulator row ----------------
+  __syncwarp();
+  if (nkt > 0) tc_wait(accf, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const int r = m0 + warp * 32 + lane;
+  float* D = optr_w<float>(p.D, b);
+  const float* Cin = (p.beta != 0.0 && p.splits == 1) ? optr<float>(p.Cin, b) : nullptr;
+  float* part = p.splits > 1
+                    ? reinterpret_cast<float*>(p.part) + (int64_t(split) * p.batch + b) * int64_t(p.M) * p.N
+                    : nullptr;
+  const float alpha = float(p.alpha), beta = float(p.beta);
+#pragma unroll 1
+  for (int cb = 0; cb < TC_BN; cb += 32) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(cb);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+          "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    if (r < p.M) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int c = n0 + cb + j;
+        const float acc = nkt > 0 ? __uint_as_float(v[j]) : 0.f;
+        if (c < p.N && (!p.tril || r + p.tril - 1 >= c)) {
+          if (part) {
+            part[r + int64_t(c) * p.M] = acc;
+          } else {
+            float o = alpha * acc;
+            if (Cin) o += beta * Cin[r + int64_t(c) * p.Cin.ld];
+            D[r + int64_t(c) * p.D.ld] = o;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tmem));
+}
+
+}  // namespace cd
