@@ -143,6 +143,13 @@ size_t cd_workspace_size_host(cd_op op, cd_dtype dt, int64_t n, const cd_opts* o
 int cd_chol_host(cd_op op, cd_dtype dt, int64_t n, const void* L_host, void* A_host,
                  const cd_opts* opts, void* ws, size_t ws_bytes, cd_stream_t stream);
 
+/* Diagnostic entry point (kernel validation): C = alpha * op(A) op(B) + beta * C with the
+ * library's Level-3 kernel family (op = transpose when ta / tb = 1), column-major, device
+ * pointers, one matrix; `ws` >= 304*128*128*sizeof(element) bytes (split-K partials). */
+int cd_debug_gemm(cd_dtype dt, int64_t M, int64_t N, int64_t K, int ta, int tb, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, void* C, int64_t ldc, double alpha, double beta, void* ws,
+                  size_t ws_bytes, cd_stream_t stream);
+
 const char* cd_status_string(int status);
 const char* cd_last_cuda_error(void); /* text of the last CUDA error seen by this thread */
 int cd_version(void);

@@ -1,8 +1,9 @@
 // choldiff.cu -- C ABI (include/choldiff.h) and host drivers of libcholdiff.so.
 //
 // Dispatch (per call):
-//   n <= 32          one warp per matrix            (sweep_warp.cuh)   PAPER.md:566-578 / 489-498
-//   n <= CTA_NMAX    one CTA per matrix             (sweep_cta.cuh)
+//   n <= 32          one warp per matrix: fp64 reverse register-resident on DMMA tiles
+//                    (sweep_reg32.cuh), otherwise sweep_warp.cuh     PAPER.md:566-578 / 489-498
+//   n <= DC_NMAX     one CTA per matrix on DMMA tiles (sweep_dmma_cta.cuh)
 //   larger n         blocked sweep (PAPER.md:689-701 reverse, 655-666 forward):
 //                    diagonal-block inverses (k_trinv) once per call, then per block
 //                    step the Level-3 updates as DMMA GEMMs (gemm.cuh) around the
@@ -28,9 +29,7 @@
 #include "gemm_tma.cuh"
 #include "gemm_tc32.cuh"
 #include "misc.cuh"
-#include "sweep_cta.cuh"
 #include "sweep_warp.cuh"
-#include "sweep_dmma32.cuh"
 #include "sweep_reg32.cuh"
 #include "sweep_dmma_cta.cuh"
 
@@ -78,7 +77,6 @@ struct LaStreams {
 };
 static thread_local LaStreams g_la[64];
 static bool g_no_lookahead = getenv("CD_NO_LOOKAHEAD") != nullptr;
-static bool g_reg32 = getenv("CD_SMEM32") == nullptr;  // register-resident small-n kernel (default)
 
 static LaStreams* la_streams() {
   int dev = 0;
@@ -185,7 +183,7 @@ static bool make_tmap(CUtensorMap* map, int* shift, const void* p, int64_t rows,
 
 // fp32 map with 128-byte swizzle for the tcgen05 kernel (gemm_tc32.cuh)
 static bool make_tmap_f32_sw128(CUtensorMap* map, const void* p, int64_t rows, int64_t cols, int64_t ld,
-                                int64_t bstride, int64_t batch, int box0, int box1) {
+                                int64_t bstride, int64_t batch, int box0, int box1, bool atom32) {
   auto enc = tmap_encoder();
   if (!enc || rows <= 0 || cols <= 0) return false;
   if (reinterpret_cast<uintptr_t>(p) % 16) return false;
@@ -196,8 +194,8 @@ static bool make_tmap_f32_sw128(CUtensorMap* map, const void* p, int64_t rows, i
   cuuint32_t es[3] = {1, 1, 1};
   const cuuint32_t rank = batch > 1 ? 3 : 2;
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(p), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
@@ -329,10 +327,10 @@ struct Gemm {
       if (sg.A.arr || sg.B.arr) return false;
       const T* pa = static_cast<const T*>(sg.A.base) + sg.A.off;
       const T* pb = static_cast<const T*>(sg.B.base) + sg.B.off;
-      const bool okA = A_ == 0 ? make_tmap_f32_sw128(&tm.a[s], pa, p.M, sg.K, sg.A.ld, sg.A.stride, p.batch, 32, 32)
-                               : make_tmap_f32_sw128(&tm.a[s], pa, sg.K, p.M, sg.A.ld, sg.A.stride, p.batch, 32, 128);
-      const bool okB = B_ == 0 ? make_tmap_f32_sw128(&tm.b[s], pb, sg.K, p.N, sg.B.ld, sg.B.stride, p.batch, 32, 128)
-                               : make_tmap_f32_sw128(&tm.b[s], pb, p.N, sg.K, sg.B.ld, sg.B.stride, p.batch, 32, 32);
+      const bool okA = A_ == 0 ? make_tmap_f32_sw128(&tm.a[s], pa, p.M, sg.K, sg.A.ld, sg.A.stride, p.batch, 32, 32, true)
+                               : make_tmap_f32_sw128(&tm.a[s], pa, sg.K, p.M, sg.A.ld, sg.A.stride, p.batch, 32, 128, false);
+      const bool okB = B_ == 0 ? make_tmap_f32_sw128(&tm.b[s], pb, sg.K, p.N, sg.B.ld, sg.B.stride, p.batch, 32, 128, false)
+                               : make_tmap_f32_sw128(&tm.b[s], pb, p.N, sg.K, sg.B.ld, sg.B.stride, p.batch, 32, 32, true);
       if (!okA || !okB) return false;
     }
     auto kern = k_gemm_tc32<A_, B_>;
@@ -387,33 +385,19 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
     const size_t smem = sweep_warp_smem<T>();
     const unsigned grid = unsigned((batch + SW_WPB - 1) / SW_WPB);
     if (rev && sizeof(T) == 8) {
-      // fp64 reverse: blocked N_b = 8 sweep on DMMA tiles (sweep_dmma32.cuh)
-      const size_t sm2 = dmma32_smem();
-      // persistent grid: enough CTAs for every SM's shared-memory-limited residency
-      const int per_sm = std::max<int>(1, int((227 * 1024) / (sm2 + 1024)));
-      const unsigned g2 = unsigned(std::min<int64_t>((batch + D32_WPB - 1) / D32_WPB, int64_t(c.sms) * per_sm));
-      const Opnd Lo = L, Ao = A;
-      auto go = [&](auto kern) {
-        set_smem(kern, sm2);
-        kern<<<g2, D32_WPB * 32, sm2, c.st>>>(n, batch, Lo, Ao, out_mode, info);
-      };
+      // fp64 reverse: register-resident N_b = 8 blocked sweep on DMMA tiles (sweep_reg32.cuh)
       const int nblk = (n + 7) / 8;
-      if (g_reg32) {
-        // register-resident variant (sweep_reg32.cuh)
-        const size_t sm3 = reg32_smem();
-        const unsigned g3 = unsigned(std::min<int64_t>((batch + R32_WPB - 1) / R32_WPB, int64_t(c.sms) * 16));
-        auto go3 = [&](auto kern) {
-          set_smem(kern, sm3);
-          kern<<<g3, R32_WPB * 32, sm3, c.st>>>(n, batch, Lo, Ao, out_mode, info);
-        };
-        if (nblk == 1) go3(k_rev_reg32<1>);
-        else if (nblk == 2) go3(k_rev_reg32<2>);
-        else if (nblk == 3) go3(k_rev_reg32<3>);
-        else go3(k_rev_reg32<4>);
-      } else if (nblk == 1) go(k_rev_dmma32<1>);
-      else if (nblk == 2) go(k_rev_dmma32<2>);
-      else if (nblk == 3) go(k_rev_dmma32<3>);
-      else go(k_rev_dmma32<4>);
+      const size_t sm3 = reg32_smem();
+      const unsigned g3 = unsigned(std::min<int64_t>((batch + R32_WPB - 1) / R32_WPB, int64_t(c.sms) * 16));
+      const Opnd Lo = L, Ao = A;
+      auto go3 = [&](auto kern) {
+        set_smem(kern, sm3);
+        kern<<<g3, R32_WPB * 32, sm3, c.st>>>(n, batch, Lo, Ao, out_mode, info);
+      };
+      if (nblk == 1) go3(k_rev_reg32<1>);
+      else if (nblk == 2) go3(k_rev_reg32<2>);
+      else if (nblk == 3) go3(k_rev_reg32<3>);
+      else go3(k_rev_reg32<4>);
     } else if (rev) {
       set_smem(k_sweep_warp_rev<T>, smem);
       k_sweep_warp_rev<T><<<grid, SW_WPB * 32, smem, c.st>>>(n, batch, L, A, out_mode, info);
@@ -428,36 +412,15 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
       k_sym2<T><<<grid_1d(total, 256, c.sms), 256, 0, c.st>>>(n, batch, A, S, rev ? 0 : 1);
       c.launched();
     }
-  } else if (rev && sizeof(T) == 8) {
-    // fp64 reverse, 32 < n <= 128: N_b = 8 blocked sweep on DMMA tiles, one CTA per matrix
-    const int nblk = (n + 7) / 8;
-    auto go = [&](auto kern, size_t smem) {
-      set_smem(kern, smem);
-      kern<<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
-    };
-    switch (nblk) {
-      case 5: go(k_rev_dmma_cta<5>, dmma_cta_smem<5>()); break;
-      case 6: go(k_rev_dmma_cta<6>, dmma_cta_smem<6>()); break;
-      case 7: go(k_rev_dmma_cta<7>, dmma_cta_smem<7>()); break;
-      case 8: go(k_rev_dmma_cta<8>, dmma_cta_smem<8>()); break;
-      case 9: go(k_rev_dmma_cta<9>, dmma_cta_smem<9>()); break;
-      case 10: go(k_rev_dmma_cta<10>, dmma_cta_smem<10>()); break;
-      case 11: go(k_rev_dmma_cta<11>, dmma_cta_smem<11>()); break;
-      case 12: go(k_rev_dmma_cta<12>, dmma_cta_smem<12>()); break;
-      case 13: go(k_rev_dmma_cta<13>, dmma_cta_smem<13>()); break;
-      case 14: go(k_rev_dmma_cta<14>, dmma_cta_smem<14>()); break;
-      case 15: go(k_rev_dmma_cta<15>, dmma_cta_smem<15>()); break;
-      default: go(k_rev_dmma_cta<16>, dmma_cta_smem<16>()); break;
-    }
-    c.launched();
   } else {
-    const size_t smem = sweep_cta_smem<T>(n);
+    // 32 < n <= 128: N_b = 8 blocked sweep on DMMA tiles (fp64 arithmetic), one CTA per matrix
+    const size_t smem = dmma_cta_smem((n + 7) / 8);
     if (rev) {
-      set_smem(k_sweep_cta_rev<T>, smem);
-      k_sweep_cta_rev<T><<<unsigned(batch), CTA_REV_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+      set_smem(k_rev_dmma_cta<T>, smem);
+      k_rev_dmma_cta<T><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
     } else {
-      set_smem(k_sweep_cta_fwd<T>, smem);
-      k_sweep_cta_fwd<T><<<unsigned(batch), CTA_THREADS, smem, c.st>>>(n, L, A, S, info);
+      set_smem(k_fwd_dmma_cta<T>, smem);
+      k_fwd_dmma_cta<T><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, S, info);
     }
     c.launched();
   }
@@ -467,11 +430,11 @@ template <typename T>
 static void run_trinv(Ctx& c, int n, int nb, bool reverse, int64_t batch, Opnd L, T* Dinv) {
   if (c.plan || !c.ok()) return;
   const int nblk = nblocks(n, nb);
-  const size_t smem = size_t(nb) * (nb + 1) / 2 * sizeof(T);
-  set_smem(k_trinv<T>, smem);
+  const size_t smem = dmma_cta_smem((nb + 7) / 8);
+  set_smem(k_trinv_dmma<T>, smem);
   c.pre(CD_PROF_TRINV, 0.0);
-  k_trinv<T><<<dim3(nblk, unsigned(batch)), TRINV_THREADS, smem, c.st>>>(n, nb, reverse ? 1 : 0, L, Dinv, nb,
-                                                                        int64_t(nb) * nb);
+  k_trinv_dmma<T><<<dim3(nblk, unsigned(batch)), DC_THREADS, smem, c.st>>>(n, nb, reverse ? 1 : 0, L, Dinv, nb,
+                                                                          int64_t(nb) * nb);
   c.launched();
 }
 
@@ -534,7 +497,7 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
           .flops(double(w) * (w + 1) * p)  // lower triangle only
           .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
     }
-    // Dbar <- chol_unblocked_rev(D, Dbar)  (+ S = Dbar + Dbar^T)      (w <= CTA_NMAX)
+    // Dbar <- chol_unblocked_rev(D, Dbar)  (+ S = Dbar + Dbar^T)      (w <= DC_NMAX)
     run_sweep_small<T>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, q > 0 ? S : null_opnd(), nullptr);
     // Rbar <- Rbar - Cbar^T B - (Dbar + Dbar^T) R
     if (q > 0) {
@@ -705,12 +668,12 @@ template <typename T>
 static void drive(Ctx& c, const Call& k) {
   const int n = int(k.n);
   if (n == 0 || k.batch == 0) return;
-  if (n <= CTA_NMAX) {
+  if (n <= DC_NMAX) {
     run_sweep_small<T>(c, k.op == CD_OP_REV, n, k.batch, k.L, k.A, k.o.out_mode, null_opnd(), k.info);
     return;
   }
   const int nb = std::min(n, k.o.nb > 0 ? k.o.nb : default_nb(k.dt, n));
-  if (nb > CTA_NMAX) {  // diagonal blocks must fit the on-chip sweep / inverse kernels
+  if (nb > DC_NMAX) {  // diagonal blocks must fit the on-chip sweep / inverse kernels
     c.err = CD_ERR_UNSUPPORTED;
     return;
   }
@@ -909,6 +872,28 @@ int cd_chol_host(cd_op op, cd_dtype dt, int64_t n, const void* L_host, void* A_h
                         : cd_chol_fwd(dt, n, dL, n, dA, n, opts, ws2, ws2b, nullptr, stream);
   if (r) return r;
   return note_cuda(cudaMemcpyAsync(A_host, dA, size_t(n) * n * es, cudaMemcpyDeviceToHost, st));
+}
+
+int cd_debug_gemm(cd_dtype dt, int64_t M, int64_t N, int64_t K, int ta, int tb, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, void* C, int64_t ldc, double alpha, double beta, void* ws, size_t ws_bytes,
+                  cd_stream_t stream) {
+  if (dt != CD_F64 && dt != CD_F32) return -1;
+  if (M < 0 || N < 0 || K < 0) return -2;
+  if (ta < 0 || ta > 1 || tb < 0 || tb > 1) return -5;
+  const size_t es = dt == CD_F64 ? 8 : 4;
+  const size_t need = size_t(PART_TILES) * G_BM * G_BN * es;
+  if (!ws || ws_bytes < need) return -16;
+  Ctx c;
+  c.plan = false;
+  c.ws = static_cast<char*>(ws);
+  c.st = reinterpret_cast<cudaStream_t>(stream);
+  c.sms = sm_count();
+  const Opnd Ao{A, nullptr, 0, lda, 0}, Bo{B, nullptr, 0, ldb, 0}, Co{C, nullptr, 0, ldc, 0};
+  if (dt == CD_F64)
+    Gemm<double>(c, int(M), int(N), ta, tb, 1).seg(Ao, Bo, int(K)).run(Co, Co, alpha, beta, 0, static_cast<double*>(ws));
+  else
+    Gemm<float>(c, int(M), int(N), ta, tb, 1).seg(Ao, Bo, int(K)).run(Co, Co, alpha, beta, 0, static_cast<float*>(ws));
+  return c.err;
 }
 
 const char* cd_status_string(int status) {

@@ -9,8 +9,9 @@
 //                   column-major stores, alpha/beta, tril mask, split-K partials)
 //
 // Operand layouts: K-contiguous operands use the K-major SW128 canonical layout (one
-// TMA box of 32 x 128); M/N-contiguous operands use the MN-major SW128 layout (four TMA
-// boxes of 32 x 32).  TF32 operands (10-bit mantissa, products accumulated in fp32):
+// TMA box of 32 x 128, 128-byte swizzle); M/N-contiguous operands use the MN-major
+// SW128-with-32-byte-atoms layout (four TMA boxes of 32 x 32, SWIZZLE_128B_ATOM_32B),
+// the only MN-major layout tcgen05 accepts for tf32.  TF32 operands (10-bit mantissa, products accumulated in fp32):
 // DESIGN.md §6 gives the error budget against the 1e-4 gate.  Same GemmParams
 // semantics as k_gemm / k_gemm_tma.
 #pragma once
@@ -28,13 +29,15 @@ constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32;
 constexpr uint32_t TC_STAGE_BYTES = (TC_BM + TC_BN) * TC_BK * 4;  // 32 KB
 constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + 1024 + 256;
 
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// shared-memory matrix descriptor; layout 2 = SWIZZLE_128B (K-major operands),
+// 1 = SWIZZLE_128B_BASE32B (MN-major tf32 operands: the only MN-major layout for tf32)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= uint64_t((saddr >> 4) & 0x3FFF);
   d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
   d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
   d |= uint64_t(1) << 46;  // descriptor version (Blackwell)
-  d |= uint64_t(2) << 61;  // SWIZZLE_128B
+  d |= uint64_t(layout & 7) << 61;
   return d;
 }
 
@@ -146,9 +149,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc32(const GemmParams p,
       const uint32_t sb = smem_u32(Bs + s * (TC_BN * TC_BK * 4));
 #pragma unroll
       for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        // K-major: advance 32 B along K inside the swizzle atom; MN-major: next 8-row K group (1 KB)
-        const uint64_t da = (TA == 0) ? umma_desc(sa + kk * 1024, 4096, 1024) : umma_desc(sa + kk * 32, 16, 1024);
-        const uint64_t db = (TB == 1) ? umma_desc(sb + kk * 1024, 4096, 1024) : umma_desc(sb + kk * 32, 16, 1024);
+        // K-major (SW128): advance 32 B along K inside the swizzle atom, 8-row groups 1 KB apart.
+        // MN-major (SW128 with 32 B atoms): K rows 128 B apart, 4-row groups 512 B apart,
+        // 32-element MN chunks 4 KB apart; each K = 8 step starts 8 rows (1 KB) further.
+        const uint64_t da = (TA == 0) ? umma_desc(sa + kk * 1024, 4096, 512, 1) : umma_desc(sa + kk * 32, 16, 1024, 2);
+        const uint64_t db = (TB == 1) ? umma_desc(sb + kk * 1024, 4096, 512, 1) : umma_desc(sb + kk * 32, 16, 1024, 2);
         const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
         asm volatile(
             "{\n.reg .pred P;\nsetp.ne.b32 P, %4, 0;\n"

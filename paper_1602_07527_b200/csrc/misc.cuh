@@ -1,6 +1,5 @@
-// misc.cuh -- small kernels of the blocked sweeps: diagonal-block inverses (the panel
-// solves C D^{-1} / C D^{-T} of PAPER.md:695, 664 become GEMMs with D^{-1}), copies,
-// output-convention epilogues (Eq. 9 mirror / GRAD) and status.
+// misc.cuh -- small kernels of the blocked sweeps: block partition, copies, output-
+// convention epilogues (Eq. 9 mirror / GRAD) and status.
 #pragma once
 #include "common.cuh"
 
@@ -21,59 +20,6 @@ __host__ __device__ inline void block_range(int n, int nb, bool reverse, int q, 
   } else {
     j0 = r + (q - 1) * nb;
     w = nb;
-  }
-}
-
-constexpr int TRINV_THREADS = 512;
-constexpr int CTA_NMAX_TRINV = 128;  // widest diagonal block inverted on chip
-
-// Dinv[b][q] = inverse of tril(L[j0:j0+w, j0:j0+w]), dense w x w (ld = ldi), upper zero.
-// Column c of X = D^{-1} solves D x = e_c by forward substitution; one warp per column,
-// lanes own rows, x_t broadcast with a shuffle.  grid = (nblk, batch).
-template <typename T>
-__global__ void __launch_bounds__(TRINV_THREADS)
-    k_trinv(int n, int nb, int reverse, Opnd Ld, T* __restrict__ Dinv, int64_t ldi, int64_t stride_blk) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sD = reinterpret_cast<T*>(smem_raw);
-  const int q = blockIdx.x;
-  const int64_t b = blockIdx.y;
-  int j0, w;
-  block_range(n, nb, reverse != 0, q, j0, w);
-  const T* L = optr<T>(Ld, b);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int m = warp; m < w; m += nw) {
-    const int cs = tri_col(w, m);
-    for (int i = m + lane; i < w; i += 32)
-      cp_async_zfill<sizeof(T)>(sD + cs + i - m, L + (j0 + i) + int64_t(j0 + m) * Ld.ld, true);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  T* X = Dinv + (int64_t(b) * gridDim.x + q) * stride_blk;
-  for (int c = warp; c < w; c += nw) {
-    T x[CTA_NMAX_TRINV / 32];
-    // rhs = e_c restricted to rows >= c; rows r = c + lane + 32u
-#pragma unroll
-    for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u) x[u] = (lane == 0 && u == 0) ? T(1) : T(0);
-    for (int t = c; t < w; ++t) {
-      const int u_t = (t - c) >> 5, l_t = (t - c) & 31;
-      T xt = T(0);
-#pragma unroll
-      for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u)
-        if (u == u_t) xt = x[u];
-      xt = __shfl_sync(0xffffffffu, xt, l_t) / sD[tri_col(w, t)];
-#pragma unroll
-      for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u) {
-        const int r = c + lane + 32 * u;
-        if (u == u_t && lane == l_t) x[u] = xt;
-        else if (r > t && r < w) x[u] -= sD[tri_col(w, t) + r - t] * xt;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < CTA_NMAX_TRINV / 32; ++u) {
-      const int r = c + lane + 32 * u;
-      if (r < w) X[r + int64_t(c) * ldi] = x[u];
-    }
-    for (int r = lane; r < c; r += 32) X[r + int64_t(c) * ldi] = T(0);
   }
 }
 

@@ -1,88 +1,75 @@
-// sweep_dmma_cta.cuh -- fp64 reverse mode for one matrix / diagonal block with n <= 128,
-// one CTA (8 warps) per matrix: the blocked reverse sweep of PAPER.md:689-701 with
-// N_b = 8 on DMMA tiles (mma.sync.m8n8k4.f64), the 8x8 diagonal blocks by Eq. 10
-// (as the paper's own implementation does).
-// Same tile arithmetic as sweep_dmma32.cuh (see there), with the tiles of each
-// update distributed over the warps of the CTA:
+// sweep_dmma_cta.cuh -- on-chip kernels for one matrix / diagonal block with n <= 128,
+// one CTA (8 warps) each, built on 8x8 DMMA tiles (mma.sync.m8n8k4.f64) held in shared
+// memory.  Arithmetic is fp64 for both fp64 and fp32 inputs (fp32 is converted on load /
+// store; the fp64 tensor cores make this cheaper than a SIMT fp32 sweep).
 //
-//   for J = NBLK-1 .. 0:   s1  Cbar <- Cbar D^{-1}            tiles over warps
-//                          s2  Bbar <- Bbar - Cbar R          tiles over warps
-//                          s3  Dbar <- Dbar - tril(Cbar^T C)  one warp (two accumulators)
-//                          s4  Dbar <- Phi(D^{-T}(P+P^T)D^{-1}), S = D^{-T}(P+P^T)D^{-1}
-//                          s5  Rbar <- Rbar - Cbar^T B - S R  tiles over warps
+//  k_rev_dmma_cta   reverse sweep: the blocked reverse of PAPER.md:689-701 with N_b = 8,
+//                   diagonal 8x8 tiles by Eq. 10 (the paper's own choice
+//                   for diagonal blocks):
+//                     s1 Cbar <- Cbar D^{-1};  s2 Bbar <- Bbar - Cbar R;
+//                     s3 Dbar <- Dbar - tril(Cbar^T C);
+//                     s4 Dbar <- Phi(D^{-T}(P+P^T)D^{-1}), P = Phi(D^T Dbar), S = D^{-T}(P+P^T)D^{-1};
+//                     s5 Rbar <- Rbar - Cbar^T B - S R
+//  k_fwd_dmma_cta   forward sweep: the blocked forward of PAPER.md:655-666 with N_b = 8,
+//                   diagonal 8x8 tiles by Eq. 8:
+//                     f1 Ddot <- Ddot - tril(Rdot R^T + R Rdot^T)
+//                     f2 Ddot <- D Phi(D^{-1} Ddot D^{-T})              (Ddot read as symmetric)
+//                     f3 Cdot <- Cdot - Bdot R^T - B Rdot^T
+//                     f4 Cdot <- (Cdot - C Ddot^T) D^{-T}
+//  k_trinv_dmma     inverse of a lower-triangular block (the panel solves of the blocked
+//                   sweeps, run as GEMMs against it):
+//                     X(J,J) = D_J^{-1};  X(I,J) = -D_I^{-1} sum_{K=J}^{I-1} D(I,K) X(K,J)
 //
-// This is the diagonal-block kernel of the blocked driver (N_b = 128 -> 16 tiles) and
-// the single / batched kernel for 32 < n <= 128.  Shared memory: the lower 8x8 tiles
-// of L and Abar, tile-packed and swizzled (bank-conflict-free fragments), 139 KB at
-// n = 128.
+// Tiles of every update are distributed over the warps.  Shared memory holds the lower
+// 8x8 tiles, tile-packed, with an XOR swizzle that makes every A / B fragment load
+// bank-conflict free (139 KB for two 128 x 128 triangles).
 #pragma once
 #include "common.cuh"
-#include "gemm.cuh"          // dmma884
+#include "gemm.cuh"  // dmma884
 
 namespace cd {
 
-// offset of element (r, c) inside a swizzled 8x8 tile: (r, c) at c*8 + (r ^ 4*((c>>1)&1)),
-// which makes every A / B fragment load of mma.m8n8k4 bank-conflict free
+// offset of element (r, c) inside a swizzled 8x8 tile: (r, c) at c*8 + (r ^ 4*((c>>1)&1))
 __device__ __forceinline__ int t8(int r, int c) { return c * 8 + (r ^ ((c & 2) << 1)); }
 
-template <int NBLK>
-__device__ __forceinline__ int tile_base(int bi, int bj) {  // lower tile (bi >= bj), column-major tile order
+// lower tile (bi >= bj) of an NBLK x NBLK tiling, column-major tile order
+__device__ __forceinline__ int tile_base(int NBLK, int bi, int bj) {
   return (bj * NBLK - (bj * (bj - 1)) / 2 + (bi - bj)) * 64;
 }
+__device__ __forceinline__ int tat(int NBLK, int i, int m) {
+  return tile_base(NBLK, i >> 3, m >> 3) + t8(i & 7, m & 7);
+}
 
+constexpr int DC_NMAX = 128;  // largest n (and diagonal block) handled on chip
 constexpr int DC_WARPS = 8;
 constexpr int DC_THREADS = DC_WARPS * 32;
 
-template <int NBLK>
-inline size_t dmma_cta_smem() {
-  constexpr int ntile = NBLK * (NBLK + 1) / 2;
+inline size_t dmma_cta_smem(int NBLK) {
+  const int ntile = NBLK * (NBLK + 1) / 2;
   return size_t(2 * ntile * 64 + NBLK * 64 + 2 * 64 + 8 * NBLK) * sizeof(double) + 16;
 }
 
-template <int NBLK>
-__global__ void __launch_bounds__(DC_THREADS, 1)
-    k_rev_dmma_cta(int n, Opnd Ld, Opnd Ad, int out_mode, Opnd Sd, int* __restrict__ info) {
-  constexpr int NP = 8 * NBLK;
-  constexpr int NTILE = NBLK * (NBLK + 1) / 2;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* sL = reinterpret_cast<double*>(smem_raw);
-  double* sA = sL + NTILE * 64;
-  double* sDi = sA + NTILE * 64;
-  double* sX = sDi + NBLK * 64;
-  double* sS = sX + 64;
-  double* sRd = sS + 64;
-  int* sbad = reinterpret_cast<int*>(sRd + NP);
+// Stage tril of an n x n column-major matrix into swizzled tiles (fp64), zero the upper
+// parts of the diagonal tiles, pad beyond n with the identity (ident) or zeros.
+template <typename TIO>
+__device__ __forceinline__ void dc_stage(int NBLK, const TIO* __restrict__ g, int64_t ld, int n, double* s,
+                                         bool ident) {
+  const int NP = 8 * NBLK, NTILE = NBLK * (NBLK + 1) / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int64_t b = blockIdx.x;
-  const double* L = optr<double>(Ld, b);
-  double* A = optr_w<double>(Ad, b);
-  auto at = [](int i, int m) { return tile_base<NBLK>(i >> 3, m >> 3) + t8(i & 7, m & 7); };
-
-  if (tid == 0) *sbad = 0x7fffffff;
-  // ---- stage the lower triangles (one column per warp pass, lanes over rows)
   for (int m = warp; m < n; m += DC_WARPS)
     for (int i = m + lane; i < n; i += 32) {
-      const int o = at(i, m);
-      cp_async_zfill<8>(sL + o, L + i + int64_t(m) * Ld.ld, true);
-      cp_async_zfill<8>(sA + o, A + i + int64_t(m) * Ad.ld, true);
+      if constexpr (sizeof(TIO) == 8) cp_async_zfill<8>(s + tat(NBLK, i, m), g + i + int64_t(m) * ld, true);
+      else s[tat(NBLK, i, m)] = double(g[i + int64_t(m) * ld]);
     }
-  // upper triangles of the diagonal tiles -> 0; padding beyond n -> blockdiag(I) / 0
   for (int e = tid; e < NBLK * 64; e += DC_THREADS) {
     const int blk = e >> 6, r = e & 7, c = (e >> 3) & 7;
     const int i = 8 * blk + r, m = 8 * blk + c;
-    const int o = tile_base<NBLK>(blk, blk) + t8(r, c);
-    if (r < c) {
-      sL[o] = 0.0;
-      sA[o] = 0.0;
-    } else if (i >= n) {
-      sL[o] = (i == m) ? 1.0 : 0.0;
-      sA[o] = 0.0;
-    }
+    const int o = tile_base(NBLK, blk, blk) + t8(r, c);
+    if (r < c) s[o] = 0.0;
+    else if (i >= n) s[o] = (ident && i == m) ? 1.0 : 0.0;
   }
   if (n < NP) {
     for (int e = tid; e < NTILE * 64; e += DC_THREADS) {
-      // decode tile index -> (bi, bj), column-major tile order
       int tix = e >> 6, bj = 0;
       while (tix >= NBLK - bj) {
         tix -= NBLK - bj;
@@ -90,27 +77,26 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
       }
       const int bi = bj + tix;
       if (bi == bj) continue;
-      const int r = e & 7, c = (e >> 3) & 7;  // note: element order inside the tile is irrelevant here
-      if (8 * bi + r >= n || 8 * bj + c >= n) {
-        sL[tile_base<NBLK>(bi, bj) + t8(r, c)] = 0.0;
-        sA[tile_base<NBLK>(bi, bj) + t8(r, c)] = 0.0;
-      }
+      const int r = e & 7, c = (e >> 3) & 7;
+      if (8 * bi + r >= n || 8 * bj + c >= n) s[tile_base(NBLK, bi, bj) + t8(r, c)] = 0.0;
     }
   }
-  cp_async_wait_all();
-  __syncthreads();
+}
+
+// 1/L_ii (sRd) and the inverse of every diagonal 8x8 tile (sDi); block-wide info.
+__device__ __forceinline__ void dc_diag_inverses(int NBLK, const double* sL, double* sDi, double* sRd, int n,
+                                                 int* sbad) {
+  const int NP = 8 * NBLK;
+  const int tid = threadIdx.x;
   for (int i = tid; i < NP; i += DC_THREADS) {
-    const double d = sL[at(i, i)];
+    const double d = sL[tat(NBLK, i, i)];
     if (i < n && bad_pivot(d)) atomicMin(sbad, i + 1);
     sRd[i] = 1.0 / d;
   }
   __syncthreads();
-  if (tid == 0 && info) info[b] = (*sbad == 0x7fffffff) ? 0 : *sbad;
-
-  // ---- D^{-1} of every diagonal 8x8 block: thread -> (block, column)
   for (int e = tid; e < NBLK * 8; e += DC_THREADS) {
     const int blk = e >> 3, c = e & 7, j0 = 8 * blk;
-    const double* D = sL + tile_base<NBLK>(blk, blk);
+    const double* D = sL + tile_base(NBLK, blk, blk);
     double x[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -130,16 +116,67 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
     for (int r = 0; r < 8; ++r) sDi[blk * 64 + t8(r, c)] = x[r];
   }
   __syncthreads();
+}
+
+// write tril (and optionally the mirror) of the tile-packed matrix to global
+template <typename TIO>
+__device__ __forceinline__ void dc_store(int NBLK, TIO* __restrict__ g, int64_t ld, int n, const double* s,
+                                         int out_mode) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int m = warp; m < n; m += DC_WARPS)
+    for (int i = m + lane; i < n; i += 32) {
+      double v = s[tat(NBLK, i, m)];
+      if (out_mode == 2 && i != m) v *= 0.5;
+      g[i + int64_t(m) * ld] = TIO(v);
+    }
+  if (out_mode != 0) {
+    for (int i = warp; i < n; i += DC_WARPS)
+      for (int m = lane; m < i; m += 32) {
+        double v = s[tat(NBLK, i, m)];
+        if (out_mode == 2) v *= 0.5;
+        g[m + int64_t(i) * ld] = TIO(v);
+      }
+  }
+}
+
+// ============================================================================ reverse
+template <typename TIO>
+__global__ void __launch_bounds__(DC_THREADS, 1)
+    k_rev_dmma_cta(int n, Opnd Ld, Opnd Ad, int out_mode, Opnd Sd, int* __restrict__ info) {
+  const int NBLK = (n + 7) >> 3;
+  const int NP = 8 * NBLK;
+  const int NTILE = NBLK * (NBLK + 1) / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sL = reinterpret_cast<double*>(smem_raw);
+  double* sA = sL + NTILE * 64;
+  double* sDi = sA + NTILE * 64;
+  double* sX = sDi + NBLK * 64;
+  double* sS = sX + 64;
+  double* sRd = sS + 64;
+  int* sbad = reinterpret_cast<int*>(sRd + NP);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t b = blockIdx.x;
+  const TIO* L = optr<TIO>(Ld, b);
+  TIO* A = optr_w<TIO>(Ad, b);
+
+  if (tid == 0) *sbad = 0x7fffffff;
+  dc_stage<TIO>(NBLK, L, Ld.ld, n, sL, true);
+  dc_stage<TIO>(NBLK, A, Ad.ld, n, sA, false);
+  cp_async_wait_all();
+  __syncthreads();
+  dc_diag_inverses(NBLK, sL, sDi, sRd, n, sbad);
+  if (tid == 0 && info) info[b] = (*sbad == 0x7fffffff) ? 0 : *sbad;
 
   for (int J = NBLK - 1; J >= 0; --J) {
     const int PT = NBLK - 1 - J, QT = J;
     const double* Di = sDi + J * 64;
-    double* Dt = sA + tile_base<NBLK>(J, J);
-    const double* Lt = sL + tile_base<NBLK>(J, J);
+    double* Dt = sA + tile_base(NBLK, J, J);
+    const double* Lt = sL + tile_base(NBLK, J, J);
 
     // s1: Cbar <- Cbar D^{-1}
     for (int rt = warp; rt < PT; rt += DC_WARPS) {
-      double* Ct = sA + tile_base<NBLK>(J + 1 + rt, J);
+      double* Ct = sA + tile_base(NBLK, J + 1 + rt, J);
       double c0 = 0.0, c1 = 0.0;
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) dmma884(c0, c1, Ct[t8(g, 4 * kk + t)], Di[t8(4 * kk + t, g)]);
@@ -153,8 +190,8 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
     if (warp == DC_WARPS - 1 && PT > 0) {
       double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
       for (int rt = 0; rt < PT; ++rt) {
-        const double* Ct = sA + tile_base<NBLK>(J + 1 + rt, J);
-        const double* Lc = sL + tile_base<NBLK>(J + 1 + rt, J);
+        const double* Ct = sA + tile_base(NBLK, J + 1 + rt, J);
+        const double* Lc = sL + tile_base(NBLK, J + 1 + rt, J);
         dmma884(a0, a1, Ct[t8(t, g)], Lc[t8(t, g)]);
         dmma884(b0, b1, Ct[t8(4 + t, g)], Lc[t8(4 + t, g)]);
       }
@@ -165,9 +202,9 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
     }
     for (int idx = warp; idx < PT * QT; idx += DC_WARPS) {
       const int rt = idx / QT, ct = idx - rt * QT;
-      const double* Ct = sA + tile_base<NBLK>(J + 1 + rt, J);
-      double* Bt = sA + tile_base<NBLK>(J + 1 + rt, ct);
-      const double* Rt = sL + tile_base<NBLK>(J, ct);
+      const double* Ct = sA + tile_base(NBLK, J + 1 + rt, J);
+      double* Bt = sA + tile_base(NBLK, J + 1 + rt, ct);
+      const double* Rt = sL + tile_base(NBLK, J, ct);
       double c0 = Bt[t8(g, 2 * t)], c1 = Bt[t8(g, 2 * t + 1)];
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) dmma884(c0, c1, Ct[t8(g, 4 * kk + t)], -Rt[t8(4 * kk + t, g)]);
@@ -212,13 +249,13 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
 
     // s5: Rbar <- Rbar - Cbar^T B - S R
     for (int ct = warp; ct < QT; ct += DC_WARPS) {
-      double* Rb = sA + tile_base<NBLK>(J, ct);
-      const double* Rt = sL + tile_base<NBLK>(J, ct);
+      double* Rb = sA + tile_base(NBLK, J, ct);
+      const double* Rt = sL + tile_base(NBLK, J, ct);
       double c0 = Rb[t8(g, 2 * t)], c1 = Rb[t8(g, 2 * t + 1)];
       double d0 = 0.0, d1 = 0.0;
       for (int rt = 0; rt < PT; ++rt) {
-        const double* Ct = sA + tile_base<NBLK>(J + 1 + rt, J);
-        const double* Bt = sL + tile_base<NBLK>(J + 1 + rt, ct);
+        const double* Ct = sA + tile_base(NBLK, J + 1 + rt, J);
+        const double* Bt = sL + tile_base(NBLK, J + 1 + rt, ct);
         dmma884(c0, c1, Ct[t8(t, g)], -Bt[t8(t, g)]);
         dmma884(d0, d1, Ct[t8(4 + t, g)], -Bt[t8(4 + t, g)]);
       }
@@ -230,28 +267,214 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
     __syncthreads();
   }
 
-  // ---- write back tril (and the requested mirror); optional dense S = Dbar + Dbar^T
-  for (int m = warp; m < n; m += DC_WARPS)
-    for (int i = m + lane; i < n; i += 32) {
-      double v = sA[at(i, m)];
-      if (out_mode == 2 && i != m) v *= 0.5;
-      A[i + int64_t(m) * Ad.ld] = v;
-    }
-  if (out_mode != 0) {
-    for (int i = warp; i < n; i += DC_WARPS)
-      for (int m = lane; m < i; m += 32) {
-        double v = sA[at(i, m)];
-        if (out_mode == 2) v *= 0.5;
-        A[m + int64_t(i) * Ad.ld] = v;
-      }
-  }
-  if (Sd.base || Sd.arr) {
-    double* S = optr_w<double>(Sd, b);
+  dc_store<TIO>(NBLK, A, Ad.ld, n, sA, out_mode);
+  if (Sd.base || Sd.arr) {  // S = Dbar + Dbar^T (diagonal doubled), dense
+    TIO* S = optr_w<TIO>(Sd, b);
     for (int e = tid; e < n * n; e += DC_THREADS) {
       const int i = e % n, c = e / n;
-      const double v = (i >= c) ? sA[at(i, c)] : sA[at(c, i)];
-      S[i + int64_t(c) * Sd.ld] = (i == c) ? 2.0 * v : v;
+      const double v = (i >= c) ? sA[tat(NBLK, i, c)] : sA[tat(NBLK, c, i)];
+      S[i + int64_t(c) * Sd.ld] = TIO((i == c) ? 2.0 * v : v);
     }
+  }
+}
+
+// ============================================================================ forward
+// Optionally writes a clean dense copy of tril(Ldot) (upper zero) to Dd, the operand of
+// Cdot <- (Cdot - C Ddot^T) D^{-T} in the blocked driver.
+template <typename TIO>
+__global__ void __launch_bounds__(DC_THREADS, 1)
+    k_fwd_dmma_cta(int n, Opnd Ld, Opnd Ad, Opnd Dd, int* __restrict__ info) {
+  const int NBLK = (n + 7) >> 3;
+  const int NP = 8 * NBLK;
+  const int NTILE = NBLK * (NBLK + 1) / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sL = reinterpret_cast<double*>(smem_raw);
+  double* sA = sL + NTILE * 64;
+  double* sDi = sA + NTILE * 64;
+  double* sX = sDi + NBLK * 64;
+  double* sY = sX + 64;
+  double* sRd = sY + 64;
+  int* sbad = reinterpret_cast<int*>(sRd + NP);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t b = blockIdx.x;
+  const TIO* L = optr<TIO>(Ld, b);
+  TIO* A = optr_w<TIO>(Ad, b);
+
+  if (tid == 0) *sbad = 0x7fffffff;
+  dc_stage<TIO>(NBLK, L, Ld.ld, n, sL, true);
+  dc_stage<TIO>(NBLK, A, Ad.ld, n, sA, false);
+  cp_async_wait_all();
+  __syncthreads();
+  dc_diag_inverses(NBLK, sL, sDi, sRd, n, sbad);
+  if (tid == 0 && info) info[b] = (*sbad == 0x7fffffff) ? 0 : *sbad;
+
+  for (int J = 0; J < NBLK; ++J) {
+    const int PT = NBLK - 1 - J, QT = J;
+    const double* Di = sDi + J * 64;
+    double* Dt = sA + tile_base(NBLK, J, J);
+    const double* Lt = sL + tile_base(NBLK, J, J);
+
+    if (warp == 0) {
+      // f1: Ddot <- Ddot - tril(Rdot R^T + R Rdot^T)
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+      for (int ct = 0; ct < QT; ++ct) {
+        const double* Rd = sA + tile_base(NBLK, J, ct);
+        const double* Rt = sL + tile_base(NBLK, J, ct);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          dmma884(c0, c1, Rd[t8(g, 4 * kk + t)], Rt[t8(g, 4 * kk + t)]);  // Rdot R^T
+          dmma884(d0, d1, Rt[t8(g, 4 * kk + t)], Rd[t8(g, 4 * kk + t)]);  // R Rdot^T
+        }
+      }
+      const int c0i = 2 * t, c1i = 2 * t + 1;
+      if (g >= c0i) Dt[t8(g, c0i)] -= c0 + d0;
+      if (g >= c1i) Dt[t8(g, c1i)] -= c1 + d1;
+      __syncwarp();
+      // f2: Ddot <- D Phi(D^{-1} Ddot D^{-T}), Ddot read as the symmetric matrix of its lower
+      //     triangle (Eq. 8 on the block)
+      double x0 = 0.0, x1 = 0.0;  // X = D^{-1} S
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int k = 4 * kk + t;
+        const double sv = (k >= g) ? Dt[t8(k, g)] : Dt[t8(g, k)];  // S(k, g)
+        dmma884(x0, x1, Di[t8(g, k)], sv);
+      }
+      sX[t8(g, c0i)] = x0;
+      sX[t8(g, c1i)] = x1;
+      __syncwarp();
+      double y0 = 0.0, y1 = 0.0;  // Y = X D^{-T}
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) dmma884(y0, y1, sX[t8(g, 4 * kk + t)], Di[t8(g, 4 * kk + t)]);
+      y0 = (g > c0i) ? y0 : (g == c0i ? 0.5 * y0 : 0.0);  // Phi
+      y1 = (g > c1i) ? y1 : (g == c1i ? 0.5 * y1 : 0.0);
+      sY[t8(g, c0i)] = y0;
+      sY[t8(g, c1i)] = y1;
+      __syncwarp();
+      double l0 = 0.0, l1 = 0.0;  // Ldot = D Phi(Y)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) dmma884(l0, l1, Lt[t8(g, 4 * kk + t)], sY[t8(4 * kk + t, g)]);
+      Dt[t8(g, c0i)] = (g >= c0i) ? l0 : 0.0;
+      Dt[t8(g, c1i)] = (g >= c1i) ? l1 : 0.0;
+    }
+    __syncthreads();
+
+    // f3 + f4 per row tile below the block
+    for (int rt = warp; rt < PT; rt += DC_WARPS) {
+      const int I = J + 1 + rt;
+      double* Ct = sA + tile_base(NBLK, I, J);
+      const double* Cl = sL + tile_base(NBLK, I, J);
+      double c0 = Ct[t8(g, 2 * t)], c1 = Ct[t8(g, 2 * t + 1)];
+      double d0 = 0.0, d1 = 0.0;
+      for (int ct = 0; ct < QT; ++ct) {
+        const double* Bd = sA + tile_base(NBLK, I, ct);
+        const double* Bl = sL + tile_base(NBLK, I, ct);
+        const double* Rd = sA + tile_base(NBLK, J, ct);
+        const double* Rt = sL + tile_base(NBLK, J, ct);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          dmma884(c0, c1, Bd[t8(g, 4 * kk + t)], -Rt[t8(g, 4 * kk + t)]);  // - Bdot R^T
+          dmma884(d0, d1, Bl[t8(g, 4 * kk + t)], -Rd[t8(g, 4 * kk + t)]);  // - B Rdot^T
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk)
+        dmma884(d0, d1, Cl[t8(g, 4 * kk + t)], -Dt[t8(g, 4 * kk + t)]);   // - C Ddot^T
+      c0 += d0;
+      c1 += d1;
+      Ct[t8(g, 2 * t)] = c0;
+      Ct[t8(g, 2 * t + 1)] = c1;
+      __syncwarp();
+      double e0 = 0.0, e1 = 0.0;  // Cdot <- Cdot D^{-T}
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) dmma884(e0, e1, Ct[t8(g, 4 * kk + t)], Di[t8(g, 4 * kk + t)]);
+      __syncwarp();
+      Ct[t8(g, 2 * t)] = e0;
+      Ct[t8(g, 2 * t + 1)] = e1;
+    }
+    __syncthreads();
+  }
+
+  dc_store<TIO>(NBLK, A, Ad.ld, n, sA, 0);
+  if (Dd.base || Dd.arr) {  // clean dense tril(Ldot)
+    TIO* Dc = optr_w<TIO>(Dd, b);
+    for (int e = tid; e < n * n; e += DC_THREADS) {
+      const int i = e % n, c = e / n;
+      Dc[i + int64_t(c) * Dd.ld] = TIO((i >= c) ? sA[tat(NBLK, i, c)] : 0.0);
+    }
+  }
+}
+
+// ============================================================================ inverse
+// Dinv[b][q] = tril(L[j0:j0+w, j0:j0+w])^{-1}, dense w x w (ld = ldi), upper zero;
+// grid = (blocks, batch); block ranges as block_range (misc.cuh).
+template <typename TIO>
+__global__ void __launch_bounds__(DC_THREADS, 1)
+    k_trinv_dmma(int n, int nb, int reverse, Opnd Ld, TIO* __restrict__ Dinv, int64_t ldi, int64_t stride_blk) {
+  const int NBLK = (nb + 7) >> 3;  // tiling of the widest block; shorter blocks are padded
+  const int NP = 8 * NBLK;
+  const int NTILE = NBLK * (NBLK + 1) / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sL = reinterpret_cast<double*>(smem_raw);
+  double* sX = sL + NTILE * 64;
+  double* sDi = sX + NTILE * 64;
+  double* sRd = sDi + NBLK * 64 + 128;
+  int* sbad = reinterpret_cast<int*>(sRd + NP);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int q = blockIdx.x;
+  const int64_t b = blockIdx.y;
+  int j0, w;
+  {
+    const int r = n % nb;
+    if (!reverse || r == 0) {
+      j0 = q * nb;
+      w = min(nb, n - j0);
+    } else if (q == 0) {
+      j0 = 0;
+      w = r;
+    } else {
+      j0 = r + (q - 1) * nb;
+      w = nb;
+    }
+  }
+  const TIO* L = optr<TIO>(Ld, b) + j0 + int64_t(j0) * Ld.ld;
+  if (tid == 0) *sbad = 0x7fffffff;
+  dc_stage<TIO>(NBLK, L, Ld.ld, w, sL, true);
+  cp_async_wait_all();
+  __syncthreads();
+  dc_diag_inverses(NBLK, sL, sDi, sRd, w, sbad);
+  // column blocks of the inverse over warps: X(J,J) = Dinv_J, then down the column
+  for (int J = warp; J < NBLK; J += DC_WARPS) {
+    double* XJJ = sX + tile_base(NBLK, J, J);
+    for (int e = lane; e < 64; e += 32) XJJ[e] = sDi[J * 64 + e];
+    __syncwarp();
+    for (int I = J + 1; I < NBLK; ++I) {
+      double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+      for (int K = J; K < I; ++K) {
+        const double* DIK = sL + tile_base(NBLK, I, K);
+        const double* XKJ = sX + tile_base(NBLK, K, J);
+        dmma884(a0, a1, DIK[t8(g, t)], XKJ[t8(t, g)]);
+        dmma884(c0, c1, DIK[t8(g, 4 + t)], XKJ[t8(4 + t, g)]);
+      }
+      double* XIJ = sX + tile_base(NBLK, I, J);
+      XIJ[t8(g, 2 * t)] = a0 + c0;  // temporary: sum D(I,K) X(K,J)
+      XIJ[t8(g, 2 * t + 1)] = a1 + c1;
+      __syncwarp();
+      double x0 = 0.0, x1 = 0.0;  // X(I,J) = -D_I^{-1} sum
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) dmma884(x0, x1, sDi[I * 64 + t8(g, 4 * kk + t)], -XIJ[t8(4 * kk + t, g)]);
+      __syncwarp();
+      XIJ[t8(g, 2 * t)] = x0;
+      XIJ[t8(g, 2 * t + 1)] = x1;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  TIO* X = Dinv + (int64_t(b) * gridDim.x + q) * stride_blk;
+  for (int e = tid; e < w * w; e += DC_THREADS) {
+    const int i = e % w, c = e / w;
+    X[i + int64_t(c) * ldi] = TIO((i >= c) ? sX[tat(NBLK, i, c)] : 0.0);
   }
 }
 

@@ -2,8 +2,8 @@
 // one WARP per matrix, the blocked reverse sweep of PAPER.md:689-701 with N_b = 8 on
 // DMMA tiles (mma.sync.m8n8k4.f64) and the 8x8 diagonal blocks by Eq. 10
 // (the paper's own choice for diagonal blocks) --
-// the same arithmetic as sweep_dmma32.cuh, but with both matrices held in REGISTERS in
-// the fragment layouts the tensor-core instructions consume:
+// the same tile arithmetic as sweep_dmma_cta.cuh, but with both matrices held in
+// REGISTERS in the fragment layouts the tensor-core instructions consume:
 //
 //   lane (g, t) = (lane >> 2, lane & 3) holds, for every lower 8x8 tile (bi, bj):
 //     L    in "T-pattern":  L(8bi + 4kk + t, 8bj + g),   kk = 0, 1   (the B operand /
