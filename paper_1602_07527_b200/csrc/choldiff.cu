@@ -32,6 +32,7 @@
 #include "sweep_warp.cuh"
 #include "sweep_reg32.cuh"
 #include "sweep_dmma_cta.cuh"
+#include "symm_ll.cuh"
 
 namespace cd {
 
@@ -600,6 +601,101 @@ static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, 
   }
 }
 
+// ------------------------------------------------------------------ blocked reverse, left-looking
+// Same arithmetic as blocked_rev, reordered: the Bbar / Rbar updates of
+// PAPER.md:696, 699 are delayed and applied to each panel just before it is processed,
+// as ONE symmetric update Cbar -= (T + T^T) L[k:n, j:k] over the finished trailing part
+// of the result (symm_ll.cuh derives it).  Per block [j, k), right to left:
+//   Cbar <- Cbar - M L[k:n, j:k]            k_symm_ll (stream-K, in-kernel fixup)
+//   Cbar <- Cbar D^{-1}                     GEMM in place
+//   Dbar <- Dbar - tril(Cbar^T C)           GEMM, tril, split-K
+//   Dbar <- chol_unblocked_rev(D, Dbar)     on-chip sweep, + S = Dbar + Dbar^T kept
+//                                           per block for later M tiles
+// Requires fp64, nb = 128 and TMA-describable Abar / L (16-byte aligned, even ld).
+static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
+
+static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, double* part_ws) {
+  const int nblk = nblocks(n, nb);
+  double* Dinv = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * nb * nb));
+  const int64_t s_stride = int64_t(LL_BM + 4) * LL_BM * nblk;
+  double* Sall = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * s_stride));
+  double* llpart = static_cast<double*>(c.take(sizeof(double) * size_t(c.sms) * 2 * LL_TILE));
+  int* cnt = static_cast<int*>(c.take(sizeof(int) * size_t(batch) * nblk));
+  if (c.plan || !c.ok()) return;
+  LLMaps tm;
+  memset(&tm, 0, sizeof(tm));
+  tm.batched = batch > 1 ? 1 : 0;
+  {
+    int sh = 0;
+    const double* Ab = static_cast<const double*>(A.base) + A.off;
+    const double* Lb = static_cast<const double*>(L.base) + L.off;
+    bool ok = make_tmap(&tm.aN, &sh, Ab, n, n, A.ld, A.stride, batch, LL_BM + 4, LL_BK) &&
+              make_tmap(&tm.aT, &sh, Ab, n, n, A.ld, A.stride, batch, LL_BK + 4, LL_BM) &&
+              make_tmap(&tm.s, &sh, Sall, LL_BM + 4, int64_t(LL_BM) * nblk, LL_BM + 4, s_stride, batch, LL_BM + 4, LL_BK) &&
+              make_tmap(&tm.l, &sh, Lb, n, n, L.ld, L.stride, batch, LL_BK + 4, LL_BN);
+    if (!ok) {
+      c.err = CD_ERR_CUDA;
+      snprintf(g_cuda_err, sizeof(g_cuda_err), "cuTensorMapEncodeTiled failed for the left-looking sweep");
+      return;
+    }
+  }
+  // the short top-left panel (w < 128): L clipped to its w columns, so the B tiles never
+  // touch L's upper triangle (the padding columns are zero-filled instead)
+  LLMaps tm_short = tm;
+  if (n % nb) {
+    int sh = 0;
+    const double* Lb = static_cast<const double*>(L.base) + L.off;
+    if (!make_tmap(&tm_short.l, &sh, Lb, n, n % nb, L.ld, L.stride, batch, LL_BK + 4, LL_BN)) {
+      c.err = CD_ERR_CUDA;
+      snprintf(g_cuda_err, sizeof(g_cuda_err), "cuTensorMapEncodeTiled failed for the left-looking sweep");
+      return;
+    }
+  }
+  c.err = note_cuda(cudaMemsetAsync(cnt, 0, sizeof(int) * size_t(batch) * nblk, c.st));
+  set_smem(k_symm_ll, LL_SMEM);
+  run_trinv<double>(c, n, nb, true, batch, L, Dinv);
+  for (int qb = nblk - 1; qb >= 0 && c.ok(); --qb) {
+    int j, w;
+    block_range(n, nb, true, qb, j, w);
+    const int k = j + w, p = n - k;
+    const Opnd Dinv_q = ws_opnd(Dinv + int64_t(qb) * nb * nb, int64_t(nblk) * nb * nb, nb);
+    const Opnd S = ws_opnd(Sall + int64_t(qb) * (LL_BM + 4) * LL_BM, s_stride, LL_BM + 4);
+    const Opnd W = sub(A, k, j);
+    if (p > 0) {
+      LLParams lp;
+      lp.A = A;
+      lp.n = n, lp.k = k, lp.j = j, lp.w = w;
+      lp.m = p / LL_BM;
+      lp.nblk = nblk;
+      lp.total = batch * int64_t(lp.m) * LL_KT_PER_BLK * lp.m;
+      lp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, lp.total / LL_KT_PER_BLK)));
+      lp.part = llpart;
+      lp.cnt = cnt;
+      c.pre(CD_PROF_GEMM, 2.0 * double(p) * p * w * double(batch));
+      if (lp.total >= (int64_t(1) << 31)) {
+        c.err = CD_ERR_UNSUPPORTED;
+        return;
+      }
+      k_symm_ll<<<lp.G, LL_THREADS, LL_SMEM, c.st>>>(lp, w < nb ? tm_short : tm);
+      c.launched();
+      Gemm<double>(c, p, w, 0, 0, batch)
+          .seg(W, Dinv_q, w)
+          .flops(double(p) * w * (w + 1))  // TRSM  Cbar D^{-1}
+          .run(null_opnd(), W, 1.0, 0.0, 0, part_ws);
+      Gemm<double>(c, w, w, 1, 0, batch)
+          .seg(W, sub(L, k, j), p)
+          .flops(double(w) * (w + 1) * p)  // lower triangle only
+          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
+    }
+    run_sweep_small<double>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, qb > 0 ? S : null_opnd(), nullptr);
+  }
+  if (info && c.ok()) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_diag_info<double><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
+    c.launched();
+  }
+}
+
 // ------------------------------------------------------------------ blocked forward
 // chol_blocked_fwd, block [j, k), w = k - j, p = n - k, q = j:
 //   Ddot <- Ddot - tril(Rdot R^T + R Rdot^T)        GEMM (2 K-segments), tril, split-K
@@ -679,11 +775,28 @@ static void drive(Ctx& c, const Call& k) {
   }
   T* part = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
   if (k.op == CD_OP_REV) {
-    // lookahead schedule needs a one-tile-wide block (in-place panel solve) and library streams
-    T* part2 = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
-    LaStreams* ls = (!g_no_lookahead && nb <= G_BN) ? (c.plan ? reinterpret_cast<LaStreams*>(1) : la_streams()) : nullptr;
-    if (ls) blocked_rev_la<T>(c, ls, n, nb, k.batch, k.L, k.A, k.info, part, part2);
-    else blocked_rev<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+    // left-looking schedule (fp64, nb = 128, TMA-describable operands); the plan sizes the
+    // workspace for both schedules because the size query does not see the pointers / ld
+    const bool ll_shape = k.dt == CD_F64 && nb == LL_BM && !g_no_ll && !g_tma_disabled && !k.L.arr && !k.A.arr;
+    const bool ll = ll_shape && (c.plan || ((reinterpret_cast<uintptr_t>(static_cast<const double*>(k.A.base) + k.A.off) % 16) == 0 &&
+                                            (reinterpret_cast<uintptr_t>(static_cast<const double*>(k.L.base) + k.L.off) % 16) == 0 &&
+                                            k.A.ld % 2 == 0 && k.L.ld % 2 == 0 &&
+                                            (k.batch == 1 || (k.A.stride % 2 == 0 && k.L.stride % 2 == 0))));
+    const size_t o0 = c.off;
+    size_t o_ll = o0;
+    if (ll) {
+      blocked_rev_ll(c, n, nb, k.batch, k.L, k.A, k.info, reinterpret_cast<double*>(part));
+      o_ll = c.off;
+      c.off = o0;
+    }
+    if (!ll || c.plan) {
+      // lookahead schedule needs a one-tile-wide block (in-place panel solve) and library streams
+      T* part2 = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
+      LaStreams* ls = (!g_no_lookahead && nb <= G_BN) ? (c.plan ? reinterpret_cast<LaStreams*>(1) : la_streams()) : nullptr;
+      if (ls) blocked_rev_la<T>(c, ls, n, nb, k.batch, k.L, k.A, k.info, part, part2);
+      else blocked_rev<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+    }
+    c.off = std::max(c.off, o_ll);
   } else {
     blocked_fwd<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
   }
@@ -711,6 +824,7 @@ static size_t plan_size(const Call& k) {
   c.plan = true;
   c.ws = nullptr;
   c.st = nullptr;
+  c.sms = sm_count();
   if (k.dt == CD_F64) drive<double>(c, k);
   else drive<float>(c, k);
   return c.off;
