@@ -257,19 +257,21 @@ def bench_single_rev(args, dist: Dist):
         "input_generation_s": round(gen_s, 1),
     }
     total_ms = sum(v[0] for v in prof.values())
-    g_ms, g_fl, g_n = prof["gemm"]
+    # dominant kernel class = the largest device-time share among the tensor-core classes
+    dom = max(("symm", "gemm", "panel"), key=lambda k: prof[k][0])
+    g_ms, g_fl, g_n = prof[dom]
     if g_n:
         per_launch_ms = g_ms / g_n
         achieved = g_fl / (g_ms * 1e-3) / 1e12
         peaks = measured_peaks()
         out["roofline"] = {
-            "kernel": "k_gemm<double> (mma.sync m8n8k4 f64 -> DMMA.8x8x4), all launches of the timed steps",
+            "kernel": KERNEL_NAMES[dom] + ", all launches of the timed steps",
             "bound": "tensor", "achieved": round(achieved, 2), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
             "peak_source": "measured fp64 DMMA issue rate on this pool (tools/microbench_fp64.cu -> "
                            "profiles/r01_microbench_fp64.txt); MEASURED_PEAKS.json has no fp64 entry",
             "frac_of_cublas_dgemm": round(achieved / CUBLAS_DGEMM_TFLOPS, 4),
-            "traffic": load_traffic("gemm"),
+            "traffic": load_traffic(dom),
             "per_launch_ms": round(per_launch_ms, 4), "launches": int(g_n),
             "share_of_step": round(g_ms / max(total_ms, 1e-9), 4),
             "whole_step_frac": round(value / dist.world / 1e3 / FP64_PEAK_TFLOPS, 4),
@@ -305,9 +307,17 @@ def bench_single_rev(args, dist: Dist):
     return out
 
 
+KERNEL_NAMES = {
+    "symm": "k_symm_ll (left-looking trailing update Cbar -= (T+T^T) L, DMMA.8x8x4 via mma.sync m8n8k4 f64, "
+            "TMA-fed, stream-K)",
+    "gemm": "k_gemm_tma<double> (mma.sync m8n8k4 f64 -> DMMA.8x8x4)",
+    "panel": "k_panel_rev (panel solve + tril correction, cooperative)",
+}
+
+
 def read_profile(Lib):
     import ctypes
-    names = {0: "gemm", 1: "splitk_reduce", 2: "sweep", 3: "trinv", 4: "other"}
+    names = {0: "gemm", 1: "splitk_reduce", 2: "sweep", 3: "trinv", 4: "other", 5: "symm", 6: "panel"}
     res = {}
     for cls, name in names.items():
         ms, fl, cnt = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()

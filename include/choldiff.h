@@ -165,9 +165,20 @@ void cd_reset_launch_count(void);
  * flop count (the paper's operation count for that update, e.g. 2*M*N*K for
  * Bbar -= Cbar R, p*w*(w+1) for the panel solve Cbar D^{-1}).  cd_profile_read
  * synchronizes the recorded events and returns, for kernel class `cls`
- * (CD_PROF_GEMM, CD_PROF_REDUCE, CD_PROF_SWEEP, CD_PROF_TRINV, CD_PROF_OTHER),
- * the summed device time (ms), flops and launch count.  Returns 0 or CD_ERR_CUDA. */
-enum { CD_PROF_GEMM = 0, CD_PROF_REDUCE = 1, CD_PROF_SWEEP = 2, CD_PROF_TRINV = 3, CD_PROF_OTHER = 4, CD_PROF_NCLS = 5 };
+ * (CD_PROF_GEMM, CD_PROF_REDUCE, CD_PROF_SWEEP, CD_PROF_TRINV, CD_PROF_OTHER,
+ * CD_PROF_SYMM = the left-looking trailing update k_symm_ll, CD_PROF_PANEL = the fused
+ * panel solve + diagonal correction k_panel_rev), the summed device time (ms), flops and
+ * launch count.  Returns 0 or CD_ERR_CUDA. */
+enum {
+  CD_PROF_GEMM = 0,
+  CD_PROF_REDUCE = 1,
+  CD_PROF_SWEEP = 2,
+  CD_PROF_TRINV = 3,
+  CD_PROF_OTHER = 4,
+  CD_PROF_SYMM = 5,
+  CD_PROF_PANEL = 6,
+  CD_PROF_NCLS = 7
+};
 void cd_profile_enable(int on);
 void cd_profile_reset(void);
 int cd_profile_read(int cls, double* ms, double* flops, int64_t* launches);

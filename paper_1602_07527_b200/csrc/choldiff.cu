@@ -33,6 +33,7 @@
 #include "sweep_reg32.cuh"
 #include "sweep_dmma_cta.cuh"
 #include "symm_ll.cuh"
+#include "panel_rev.cuh"
 
 namespace cd {
 
@@ -614,6 +615,16 @@ static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, 
 // Requires fp64, nb = 128 and TMA-describable Abar / L (16-byte aligned, even ld).
 static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
 
+static int panel_occupancy() {
+  static int occ = 0;
+  if (!occ) {
+    set_smem(k_panel_rev, PR_SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_panel_rev, PR_THREADS, PR_SMEM) != cudaSuccess || occ < 1)
+      occ = 1;
+  }
+  return occ;
+}
+
 static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, double* part_ws) {
   const int nblk = nblocks(n, nb);
   double* Dinv = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * nb * nb));
@@ -621,7 +632,10 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
   double* Sall = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * s_stride));
   double* llpart = static_cast<double*>(c.take(sizeof(double) * size_t(c.sms) * 2 * LL_TILE));
   int* cnt = static_cast<int*>(c.take(sizeof(int) * size_t(batch) * nblk));
+  double* prpart = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
+  (void)part_ws;
   if (c.plan || !c.ok()) return;
+  set_smem(k_panel_rev, PR_SMEM);
   LLMaps tm;
   memset(&tm, 0, sizeof(tm));
   tm.batched = batch > 1 ? 1 : 0;
@@ -671,21 +685,32 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       lp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, lp.total / LL_KT_PER_BLK)));
       lp.part = llpart;
       lp.cnt = cnt;
-      c.pre(CD_PROF_GEMM, 2.0 * double(p) * p * w * double(batch));
+      c.pre(CD_PROF_SYMM, 2.0 * double(p) * p * w * double(batch));
       if (lp.total >= (int64_t(1) << 31)) {
         c.err = CD_ERR_UNSUPPORTED;
         return;
       }
       k_symm_ll<<<lp.G, LL_THREADS, LL_SMEM, c.st>>>(lp, w < nb ? tm_short : tm);
       c.launched();
-      Gemm<double>(c, p, w, 0, 0, batch)
-          .seg(W, Dinv_q, w)
-          .flops(double(p) * w * (w + 1))  // TRSM  Cbar D^{-1}
-          .run(null_opnd(), W, 1.0, 0.0, 0, part_ws);
-      Gemm<double>(c, w, w, 1, 0, batch)
-          .seg(W, sub(L, k, j), p)
-          .flops(double(w) * (w + 1) * p)  // lower triangle only
-          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
+      // Cbar <- Cbar D^{-1};  Dbar <- Dbar - tril(Cbar^T C)   (one cooperative kernel)
+      PanelParams pp;
+      pp.A = A;
+      pp.L = L;
+      pp.Dinv = Dinv + int64_t(qb) * nb * nb;
+      pp.dstride = int64_t(nblk) * nb * nb;
+      pp.dld = nb;
+      pp.n = n, pp.j = j, pp.w = w, pp.k = k;
+      pp.tiles = p / LL_BM;
+      pp.batch = batch;
+      pp.part = prpart;
+      const int64_t units = batch * pp.tiles;
+      const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs (phase 2)
+      (void)units;
+      void* args[] = {&pp};
+      c.pre(CD_PROF_PANEL, double(p) * w * (w + 1) * 2.0 * double(batch));
+      c.err = note_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_panel_rev), dim3(grid),
+                                                    dim3(PR_THREADS), args, PR_SMEM, c.st));
+      c.launched();
     }
     run_sweep_small<double>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, qb > 0 ? S : null_opnd(), nullptr);
   }

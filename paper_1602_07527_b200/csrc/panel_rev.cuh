@@ -1,0 +1,249 @@
+// panel_rev.cuh -- the panel step of the blocked reverse sweep as ONE cooperative kernel
+// (fp64, DMMA):
+//
+//     Cbar <- Cbar D^{-1}                  ("solving a triangular system")
+//     Dbar <- Dbar - tril(Cbar^T C)        (only the triangle is needed,
+//                                           PAPER.md:717-723)
+//
+// for the p x w panel Cbar = Abar[k:n, j:k], C = L[k:n, j:k], D^{-1} precomputed by
+// k_trinv.  One CTA per 128-row tile of the panel (looping if there are more tiles than
+// SMs):
+//   phase 1  W = Cbar_t D^{-1} (lower-triangular D^{-1}: K chunks that cannot reach a
+//            warp's columns are skipped), stored in place and kept in shared memory;
+//            P_t = tril(W^T C_t) (warps above the diagonal skip), stored to slot t;
+//   grid sync (cooperative launch: all CTAs co-resident);
+//   phase 2  Dbar -= sum_t P_t over the lower triangle, four threads per element with a
+//            fixed summation tree (bitwise deterministic).
+// Replaces two split-K GEMM launches and their reduction launches on the critical path.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace cd {
+
+constexpr int PR_THREADS = 256;
+constexpr int PR_BK = 16;
+constexpr int PR_STAGES = 3;
+constexpr int PR_KM_PITCH = 128 + 4;  // As[k][m]
+constexpr int PR_NK_PITCH = PR_BK + 4;  // Bs[n][k]
+constexpr int PR_A_SIZE = PR_BK * PR_KM_PITCH;  // 2112
+constexpr int PR_B_SIZE = 128 * PR_NK_PITCH;    // 2560
+constexpr int PR_W_PITCH = 132;
+constexpr size_t PR_SMEM_A = size_t(PR_STAGES) * (PR_A_SIZE + PR_B_SIZE) * 8;              // step A stages
+constexpr size_t PR_SMEM_C = size_t(128) * PR_W_PITCH * 8 + size_t(PR_STAGES) * PR_B_SIZE * 8;  // W + step C stages
+constexpr size_t PR_SMEM = PR_SMEM_A > PR_SMEM_C ? PR_SMEM_A : PR_SMEM_C;
+
+struct PanelParams {
+  Opnd A, L;         // Abar and L (whole matrices)
+  const double* Dinv;  // w x w (ld dld) inverse of the diagonal block (per batch: + b * dstride)
+  int64_t dstride;
+  int dld;
+  int n, j, w, k;    // panel rows [k, n), columns [j, j + w)
+  int tiles;         // (n - k) / 128 per matrix
+  int64_t batch;
+  double* part;      // [batch * tiles][128 * 128] slots
+};
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(valid ? 8 : 0));
+}
+
+__global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_pr[];
+  double* sm = reinterpret_cast<double*>(smem_pr);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp -> (wm, wn): the SM sub-partition (warp & 3) gets one column group from each
+  // end, so the triangular work of step A is balanced across sub-partitions
+  const int wm = warp >> 2, wn = wm == 0 ? (warp & 3) : 3 - (warp & 3), g = lane >> 2, t = lane & 3;
+  const int w = p.w;
+  const int64_t units = p.batch * p.tiles;
+
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t b = u / p.tiles;
+    const int tl = int(u - b * p.tiles);
+    const int r0 = p.k + 128 * tl;
+    double* Cb = optr_w<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;     // Cbar tile (128 x w)
+    const double* Ct = optr<double>(p.L, b) + r0 + int64_t(p.j) * p.L.ld;  // C tile
+    const double* Di = p.Dinv + b * p.dstride;
+
+    // ---------------- step A: W = Cbar_t D^{-1} ----------------
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    const int nkc = (w + PR_BK - 1) / PR_BK;
+    auto load_a = [&](int st, int kc) {
+      double* as = sm + st * (PR_A_SIZE + PR_B_SIZE);
+      double* bs = as + PR_A_SIZE;
+      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
+        const int m = e & 127, kx = e >> 7;  // A: Cbar[m, kc + kx]
+        const int kk = kc * PR_BK + kx;
+        cp_async8(as + kx * PR_KM_PITCH + m, Cb + m + int64_t(min(kk, w - 1)) * p.A.ld, kk < w);
+      }
+      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
+        const int kx = e % PR_BK, nn = e / PR_BK;  // B: Dinv[kc + kx, nn]
+        const int kk = kc * PR_BK + kx;
+        const bool ok = kk < w && nn < w;
+        cp_async8(bs + nn * PR_NK_PITCH + kx, Di + (ok ? kk + int64_t(nn) * p.dld : 0), ok);
+      }
+    };
+#pragma unroll 1
+    for (int s = 0; s < PR_STAGES - 1; ++s) {
+      if (s < nkc) load_a(s, s);
+      cp_async_commit();
+    }
+#pragma unroll 1
+    for (int kc = 0; kc < nkc; ++kc) {
+      cp_async_wait<PR_STAGES - 2>();
+      __syncthreads();
+      if (kc + PR_STAGES - 1 < nkc) load_a((kc + PR_STAGES - 1) % PR_STAGES, kc + PR_STAGES - 1);
+      cp_async_commit();
+      // D^{-1}[kk, c] = 0 for kk < c: this chunk reaches columns c <= kc*16 + 15 only
+      if (kc * PR_BK + PR_BK - 1 >= wn * 32) {
+        const double* as = sm + (kc % PR_STAGES) * (PR_A_SIZE + PR_B_SIZE);
+        const double* bs = as + PR_A_SIZE;
+#pragma unroll
+        for (int kq = 0; kq < PR_BK / 4; ++kq) {
+          const int kx = kq * 4 + t;
+          double a[8], bb[4];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = as[kx * PR_KM_PITCH + wm * 64 + i * 8 + g];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[(wn * 32 + jj * 8 + g) * PR_NK_PITCH + kx];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
+        }
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();  // stage buffers dead: W and the step C stages alias them
+    double* Ws = sm;
+    double* Cs = sm + 128 * PR_W_PITCH;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wm * 64 + i * 8 + g;
+          const int c = wn * 32 + jj * 8 + 2 * t + e;
+          Ws[r + c * PR_W_PITCH] = acc[i][jj][e];  // columns >= w are exactly 0
+          if (c < w) Cb[r + int64_t(c) * p.A.ld] = acc[i][jj][e];
+        }
+
+    // ---------------- step C: P_t = tril(W^T C_t) ----------------
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    auto load_c = [&](int st, int rc) {
+      double* bs = Cs + st * PR_B_SIZE;
+      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
+        const int kx = e % PR_BK, nn = e / PR_BK;  // B: C[rc*16 + kx, nn]
+        const bool ok = nn < w;
+        cp_async8(bs + nn * PR_NK_PITCH + kx, Ct + (rc * PR_BK + kx) + int64_t(ok ? nn : 0) * p.L.ld, ok);
+      }
+    };
+    constexpr int NRC = 128 / PR_BK;
+#pragma unroll 1
+    for (int s = 0; s < PR_STAGES - 1; ++s) {
+      load_c(s, s);
+      cp_async_commit();
+    }
+    const bool active = wm * 64 + 63 >= wn * 32;  // some a >= b in this warp's tile
+#pragma unroll 1
+    for (int rc = 0; rc < NRC; ++rc) {
+      cp_async_wait<PR_STAGES - 2>();
+      __syncthreads();
+      if (rc + PR_STAGES - 1 < NRC) load_c((rc + PR_STAGES - 1) % PR_STAGES, rc + PR_STAGES - 1);
+      cp_async_commit();
+      if (active) {
+        const double* bs = Cs + (rc % PR_STAGES) * PR_B_SIZE;
+#pragma unroll
+        for (int kq = 0; kq < PR_BK / 4; ++kq) {
+          const int kx = kq * 4 + t;
+          double a[8], bb[4];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = Ws[(wm * 64 + i * 8 + g) * PR_W_PITCH + rc * PR_BK + kx];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[(wn * 32 + jj * 8 + g) * PR_NK_PITCH + kx];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
+        }
+      }
+    }
+    cp_async_wait_all();
+    double* slot = p.part + u * int64_t(128 * 128);
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = wm * 64 + i * 8 + g;
+            const int c = wn * 32 + jj * 8 + 2 * t + e;
+            if (r >= c) __stcg(slot + r + c * 128, acc[i][jj][e]);
+          }
+    }
+    __syncthreads();  // before the next tile reuses the shared memory
+  }
+
+  // ---------------- phase 2: Dbar -= sum_t P_t (lower triangle) ----------------
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  // 8 lanes per element (a warp takes 4 elements per round), each lane two independent
+  // chains over the tiles; fixed combination tree -> bitwise deterministic.  The grid is
+  // always every co-resident CTA (CTAs without a tile join here), so few tiles still
+  // spread over the whole GPU.
+  const int64_t nwarps = int64_t(gridDim.x) * (PR_THREADS / 32);
+  const int64_t gw = int64_t(blockIdx.x) * (PR_THREADS / 32) + warp;
+  const int64_t ntri = int64_t(w) * (w + 1) / 2;
+  const int64_t nel = ntri * p.batch;  // lower-triangle entries (a >= c), column-packed
+  const int q = lane & 7;
+  for (int64_t wb = gw * 4; wb < nel; wb += nwarps * 4) {
+    const int64_t el = wb + (lane >> 3);
+    const bool on = el < nel;
+    int64_t b = 0;
+    int a = 0, c = 0;
+    if (on) {
+      b = el / ntri;
+      const int rem = int(el - b * ntri);
+      // column-packed: column c starts at off(c) = c*w - c*(c-1)/2 and holds w - c entries
+      const double tw = 2.0 * w + 1.0;
+      c = int((tw - sqrt(tw * tw - 8.0 * rem)) * 0.5);
+      c = max(0, min(c, w - 1));
+      while (c > 0 && c * w - c * (c - 1) / 2 > rem) --c;
+      while (c + 1 < w && (c + 1) * w - (c + 1) * c / 2 <= rem) ++c;
+      a = c + (rem - (c * w - c * (c - 1) / 2));
+    }
+    double s0 = 0.0, s1 = 0.0;
+    if (on) {
+      const double* pb = p.part + b * p.tiles * int64_t(128 * 128) + a + c * 128;
+      int tl = q;
+      for (; tl + 8 < p.tiles; tl += 16) {
+        s0 += __ldcg(pb + int64_t(tl) * 128 * 128);
+        s1 += __ldcg(pb + int64_t(tl + 8) * 128 * 128);
+      }
+      if (tl < p.tiles) s0 += __ldcg(pb + int64_t(tl) * 128 * 128);
+    }
+    double s = s0 + s1;
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (q == 0 && on) {
+      double* D = optr_w<double>(p.A, b) + (p.j + a) + int64_t(p.j + c) * p.A.ld;
+      *D -= s;
+    }
+  }
+}
+
+}  // namespace cd
