@@ -414,7 +414,7 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
                        f"sharded by matrix over {P} GPU(s)",
            "value": round(mats, 1), "unit": "matrices/s", "ms_per_step": round(worst, 4),
            "gflops": round(mats * rev_flops(n) / 1e9, 1), "steps": args.steps_batched,
-           "roofline": {"kernel": "k_rev_dmma32<4> (one warp per matrix, N_b=8 DMMA tiles)", "bound": "hbm", "achieved": round(achieved_gbs, 1),
+           "roofline": {"kernel": "k_rev_bulk32<4> (one warp per matrix, N_b=8 DMMA tiles, cp.async-staged conflict-free smem columns)", "bound": "hbm", "achieved": round(achieved_gbs, 1),
                         "peak": hbm, "unit": "GB/s", "frac": round(achieved_gbs / hbm, 4),
                         "algorithmic_bytes_per_matrix": algo_bytes,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs", "traffic": load_traffic("batched32")},

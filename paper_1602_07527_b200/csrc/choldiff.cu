@@ -31,6 +31,7 @@
 #include "misc.cuh"
 #include "sweep_warp.cuh"
 #include "sweep_reg32.cuh"
+#include "sweep_bulk32.cuh"
 #include "sweep_dmma_cta.cuh"
 #include "symm_ll.cuh"
 #include "panel_rev.cuh"
@@ -201,6 +202,7 @@ static bool make_tmap_f32_sw128(CUtensorMap* map, const void* p, int64_t rows, i
 }
 
 static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
+static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
 
 // ------------------------------------------------------------------ GEMM launcher
 constexpr int64_t PART_TILES = 2 * 152;  // split-K partial budget, in 128x128 output tiles
@@ -386,7 +388,28 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
   if (n <= 32) {
     const size_t smem = sweep_warp_smem<T>();
     const unsigned grid = unsigned((batch + SW_WPB - 1) / SW_WPB);
-    if (rev && sizeof(T) == 8) {
+    const bool bulk_ok = rev && sizeof(T) == 8 && n % 8 == 0 && out_mode == CD_OUT_TRIL && !L.arr && !A.arr &&
+                         !S.base && !S.arr && !g_no_bulk32 && L.ld % 2 == 0 && A.ld % 2 == 0 &&
+                         (batch == 1 || (L.stride % 2 == 0 && A.stride % 2 == 0)) &&
+                         (reinterpret_cast<uintptr_t>(static_cast<const T*>(L.base) + L.off) % 16) == 0 &&
+                         (reinterpret_cast<uintptr_t>(static_cast<const T*>(A.base) + A.off) % 16) == 0;
+    if (bulk_ok) {
+      // fp64 reverse, n = 8/16/24/32: the same register sweep fed by bulk copies (sweep_bulk32.cuh)
+      const Opnd Lo = L, Ao = A;
+      const int nblk = n / 8;
+      auto launch = [&](auto kern, size_t smb) {
+        set_smem(kern, smb);
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, B32_WPB * 32, smb);
+        const unsigned gb = unsigned(std::max<int64_t>(1, std::min<int64_t>((batch + B32_WPB - 1) / B32_WPB,
+                                                                          int64_t(c.sms) * std::max(occ, 1))));
+        kern<<<gb, B32_WPB * 32, smb, c.st>>>(batch, Lo, Ao, info);
+      };
+      if (nblk == 1) launch(k_rev_bulk32<1>, b32_smem<1>());
+      else if (nblk == 2) launch(k_rev_bulk32<2>, b32_smem<2>());
+      else if (nblk == 3) launch(k_rev_bulk32<3>, b32_smem<3>());
+      else launch(k_rev_bulk32<4>, b32_smem<4>());
+    } else if (rev && sizeof(T) == 8) {
       // fp64 reverse: register-resident N_b = 8 blocked sweep on DMMA tiles (sweep_reg32.cuh)
       const int nblk = (n + 7) / 8;
       const size_t sm3 = reg32_smem();

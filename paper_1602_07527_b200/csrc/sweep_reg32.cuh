@@ -53,79 +53,22 @@ __device__ __forceinline__ void r32_transpose(double c0, double c1, int g, int t
   d1 = (g & 1) ? y1 : x1;
 }
 
-template <int NBLK>
-__global__ void __launch_bounds__(R32_WPB * 32, 3)
-    k_rev_reg32(int n, int64_t batch, Opnd Ld, Opnd Ad, int out_mode, int* __restrict__ info) {
-  constexpr int NT = NBLK * (NBLK + 1) / 2;  // lower tiles
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// The register-resident sweep proper (shared by the kernels that stage the operands
+// differently): diagonal-block inverses (+ info), then the N_b = 8 blocked reverse sweep
+// on the fragments.  dat(blk, q, r) = L(8 blk + r, 8 blk + q) (diagonal tile, column q, row r).
+template <int NBLK, class DAt>
+__device__ __forceinline__ void r32_core(double (&Lt)[NBLK * (NBLK + 1) / 2][2], double (&Ac)[NBLK * (NBLK + 1) / 2][2],
+                                         DAt dat, double* sDi, int n, int* __restrict__ info, int64_t b, int lane) {
   const int g = lane >> 2, t = lane & 3;
-  double* sD = reinterpret_cast<double*>(smem_raw) + w * R32_SMEM_PER_WARP;  // 4 diag tiles of L, col-major 8x8
-  double* sDi = sD + 4 * 64;                                                 // their inverses
-  // tile index of (bi, bj), bi >= bj, column-major tile order
   auto TI = [](int bi, int bj) { return bj * NBLK - (bj * (bj - 1)) / 2 + (bi - bj); };
-
-  for (int64_t b = int64_t(blockIdx.x) * R32_WPB + w; b < batch; b += int64_t(gridDim.x) * R32_WPB) {
-    const double* Lg = optr<double>(Ld, b);
-    double* Ag = optr_w<double>(Ad, b);
-    double Lt[NT][2], Ac[NT][2];
-    // ---- loads (lower triangles only; padding -> blockdiag(I) / 0)
-    if (n == 8 * NBLK) {  // no padding: only the diagonal tiles are masked
-#pragma unroll
-      for (int bj = 0; bj < NBLK; ++bj)
-#pragma unroll
-        for (int bi = bj; bi < NBLK; ++bi) {
-          const int ti = TI(bi, bj);
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const int r = 8 * bi + 4 * kk + t, c = 8 * bj + g;
-            Lt[ti][kk] = (bi > bj || r >= c) ? __ldg(Lg + r + int64_t(c) * Ld.ld) : 0.0;
-          }
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
-            Ac[ti][e] = (bi > bj || r >= c) ? Ag[r + int64_t(c) * Ad.ld] : 0.0;
-          }
-        }
-    } else {
-#pragma unroll
-      for (int bj = 0; bj < NBLK; ++bj)
-#pragma unroll
-        for (int bi = bj; bi < NBLK; ++bi) {
-          const int ti = TI(bi, bj);
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const int r = 8 * bi + 4 * kk + t, c = 8 * bj + g;
-            double v = 0.0;
-            if (r < n && c < n) {
-              if (r >= c) v = Lg[r + int64_t(c) * Ld.ld];
-            } else if (r == c) {
-              v = 1.0;
-            }
-            Lt[ti][kk] = v;
-          }
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
-            Ac[ti][e] = (r < n && c < n && r >= c) ? Ag[r + int64_t(c) * Ad.ld] : 0.0;
-          }
-        }
-    }
-    // ---- diagonal blocks of L -> smem (for their inverses), info
-    __syncwarp();
-#pragma unroll
-    for (int J = 0; J < NBLK; ++J)
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) sD[J * 64 + g * 8 + 4 * kk + t] = Lt[TI(J, J)][kk];  // (row 4kk+t, col g)
-    __syncwarp();
     {
       const int blk = lane >> 3, c = lane & 7;
       bool bad = false;
       {  // all lanes take part (shuffles); lanes of blocks >= NBLK work on tile 0 and discard
-        const double* D = sD + (blk < NBLK ? blk : 0) * 64;
-        bad = blk < NBLK && (8 * blk + c < n) && bad_pivot(D[c * 8 + c]);
+        const int dblk = blk < NBLK ? blk : 0;
+        bad = blk < NBLK && (8 * blk + c < n) && bad_pivot(dat(dblk, c, c));
         // 1/D(r,r), r = 0..7: each lane computes its own column's, the rest by shuffle
-        const double rdc = 1.0 / D[c * 8 + c];
+        const double rdc = 1.0 / dat(dblk, c, c);
         double x[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -136,7 +79,7 @@ __global__ void __launch_bounds__(R32_WPB * 32, 3)
             double s = (r == c) ? 1.0 : 0.0;
 #pragma unroll
             for (int q = 0; q < r; ++q)
-              if (q >= c) s -= D[q * 8 + r] * x[q];
+              if (q >= c) s -= dat(dblk, q, r) * x[q];
             x[r] = s * rdr;
           }
         }
@@ -255,6 +198,74 @@ __global__ void __launch_bounds__(R32_WPB * 32, 3)
         }
     }
 
+}
+
+template <int NBLK>
+__global__ void __launch_bounds__(R32_WPB * 32, 3)
+    k_rev_reg32(int n, int64_t batch, Opnd Ld, Opnd Ad, int out_mode, int* __restrict__ info) {
+  constexpr int NT = NBLK * (NBLK + 1) / 2;  // lower tiles
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double* sD = reinterpret_cast<double*>(smem_raw) + w * R32_SMEM_PER_WARP;  // 4 diag tiles of L, col-major 8x8
+  double* sDi = sD + 4 * 64;                                                 // their inverses
+  // tile index of (bi, bj), bi >= bj, column-major tile order
+  auto TI = [](int bi, int bj) { return bj * NBLK - (bj * (bj - 1)) / 2 + (bi - bj); };
+
+  for (int64_t b = int64_t(blockIdx.x) * R32_WPB + w; b < batch; b += int64_t(gridDim.x) * R32_WPB) {
+    const double* Lg = optr<double>(Ld, b);
+    double* Ag = optr_w<double>(Ad, b);
+    double Lt[NT][2], Ac[NT][2];
+    // ---- loads (lower triangles only; padding -> blockdiag(I) / 0)
+    if (n == 8 * NBLK) {  // no padding: only the diagonal tiles are masked
+#pragma unroll
+      for (int bj = 0; bj < NBLK; ++bj)
+#pragma unroll
+        for (int bi = bj; bi < NBLK; ++bi) {
+          const int ti = TI(bi, bj);
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int r = 8 * bi + 4 * kk + t, c = 8 * bj + g;
+            Lt[ti][kk] = (bi > bj || r >= c) ? __ldg(Lg + r + int64_t(c) * Ld.ld) : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
+            Ac[ti][e] = (bi > bj || r >= c) ? Ag[r + int64_t(c) * Ad.ld] : 0.0;
+          }
+        }
+    } else {
+#pragma unroll
+      for (int bj = 0; bj < NBLK; ++bj)
+#pragma unroll
+        for (int bi = bj; bi < NBLK; ++bi) {
+          const int ti = TI(bi, bj);
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int r = 8 * bi + 4 * kk + t, c = 8 * bj + g;
+            double v = 0.0;
+            if (r < n && c < n) {
+              if (r >= c) v = Lg[r + int64_t(c) * Ld.ld];
+            } else if (r == c) {
+              v = 1.0;
+            }
+            Lt[ti][kk] = v;
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
+            Ac[ti][e] = (r < n && c < n && r >= c) ? Ag[r + int64_t(c) * Ad.ld] : 0.0;
+          }
+        }
+    }
+    // ---- diagonal blocks of L -> smem (for their inverses), info
+    __syncwarp();
+#pragma unroll
+    for (int J = 0; J < NBLK; ++J)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) sD[J * 64 + g * 8 + 4 * kk + t] = Lt[TI(J, J)][kk];  // (row 4kk+t, col g)
+    __syncwarp();
+    r32_core<NBLK>(Lt, Ac, [&](int blk, int q, int r) { return sD[blk * 64 + q * 8 + r]; }, sDi, n, info, b, lane);
     // ---- store tril(Sigma_bar) (and the requested mirror)
     if (out_mode == 0 && n == 8 * NBLK) {
 #pragma unroll
