@@ -193,6 +193,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc32(const GemmParams p,
           "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
           "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
+    // Cin is usually D itself (in-place update): load the whole chunk first, or every
+    // store would order the next load behind it (one memory latency per column)
+    float cin[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int c = n0 + cb + j;
+      cin[j] = (Cin && r < p.M && c < p.N) ? __ldcg(Cin + r + int64_t(c) * p.Cin.ld) : 0.f;
+    }
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     if (r < p.M) {
 #pragma unroll
@@ -203,9 +211,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc32(const GemmParams p,
           if (part) {
             part[r + int64_t(c) * p.M] = acc;
           } else {
-            float o = alpha * acc;
-            if (Cin) o += beta * Cin[r + int64_t(c) * p.Cin.ld];
-            D[r + int64_t(c) * p.D.ld] = o;
+            D[r + int64_t(c) * p.D.ld] = alpha * acc + beta * cin[j];
           }
         }
       }
