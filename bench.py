@@ -417,7 +417,7 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
            "roofline": {"kernel": "k_rev_bulk32<4> (one warp per matrix, N_b=8 DMMA tiles, cp.async-staged conflict-free smem columns)", "bound": "hbm", "achieved": round(achieved_gbs, 1),
                         "peak": hbm, "unit": "GB/s", "frac": round(achieved_gbs / hbm, 4),
                         "algorithmic_bytes_per_matrix": algo_bytes,
-                        "peak_source": "MEASURED_PEAKS.json hbm_gbs", "traffic": load_traffic("batched32")},
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs", "traffic": load_traffic("bulk32")},
            "gpu_launches": int(launches), "clocks": clk.summary()}
     if gather and P > 1:
         # NCCL used only to gather the sharded results (north star), timed separately
