@@ -137,7 +137,8 @@ static int grid_1d(int64_t total, int threads, int sms) {
 // ------------------------------------------------------------------ kernel attribute setup
 template <typename K>
 static void set_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  // opt in well below 48 KB: the 48 KB default limit counts static shared memory too
+  if (bytes > 32 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
 // ------------------------------------------------------------------ TMA tensor maps

@@ -59,9 +59,10 @@ def test_nb_too_large_is_unsupported():
         cd.chol_rev(to_dev(L), to_dev(Lb), nb=256)
 
 
-@pytest.mark.parametrize("n", [17, 64, 200])
-@pytest.mark.parametrize("pad", [1, 3])
+@pytest.mark.parametrize("n", [17, 32, 64, 200, 300])
+@pytest.mark.parametrize("pad", [1, 2, 3])
 def test_leading_dimension(n, pad):
+    # odd ld -> cp.async GEMM / reg32 fallbacks; even ld -> TMA / left-looking / bulk32 paths with ld > n
     L, Lb, Sd = synthetic.draw(n, 5 * n + pad, sdot=True)
     Ld, Ad = to_dev(L, ld_pad=pad), to_dev(Lb, ld_pad=pad)
     assert Ld.stride(-1) == n + pad
@@ -72,9 +73,9 @@ def test_leading_dimension(n, pad):
     assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
 
 
-@pytest.mark.parametrize("n", [1, 5, 17, 32, 33, 64, 100, 128, 150])
+@pytest.mark.parametrize("n", [1, 5, 8, 16, 17, 24, 32, 33, 64, 100, 128, 150, 300])
 def test_strided_batched(n):
-    B = 37 if n <= 128 else 5
+    B = 37 if n <= 128 else (5 if n < 300 else 3)
     L, Lb, Sd = synthetic.draw_batch(n, B, seed=3 * n, sdot=True)
     r = cd.chol_rev(to_dev(L), to_dev(Lb))
     assert nerr(to_host(r), oracle_rev(L, Lb)) < TOL64
