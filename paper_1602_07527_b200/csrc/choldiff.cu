@@ -632,10 +632,11 @@ static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, 
 // as ONE symmetric update Cbar -= (T + T^T) L[k:n, j:k] over the finished trailing part
 // of the result (symm_ll.cuh derives it).  Per block [j, k), right to left:
 //   Cbar <- Cbar - M L[k:n, j:k]            k_symm_ll (stream-K, in-kernel fixup)
-//   Cbar <- Cbar D^{-1}                     GEMM in place
-//   Dbar <- Dbar - tril(Cbar^T C)           GEMM, tril, split-K
-//   Dbar <- chol_unblocked_rev(D, Dbar)     on-chip sweep, + S = Dbar + Dbar^T kept
-//                                           per block for later M tiles
+//   Cbar <- Cbar D^{-1}                     } k_panel_rev, one cooperative launch:
+//   Dbar <- Dbar - tril(Cbar^T C)           }   tile-parallel products + grid-wide
+//   Dbar <- chol_unblocked_rev(D, Dbar)     }   deterministic reduction; the diagonal
+//                                               block by Eq. 10, with
+//                                               S = Dbar + Dbar^T kept per block for later M tiles
 // Requires fp64, nb = 128 and TMA-describable Abar / L (16-byte aligned, even ld).
 static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
 
@@ -657,6 +658,8 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
   double* llpart = static_cast<double*>(c.take(sizeof(double) * size_t(c.sms) * 2 * LL_TILE));
   int* cnt = static_cast<int*>(c.take(sizeof(int) * size_t(batch) * nblk));
   double* prpart = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
+  double* Pws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
+  double* Zws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   (void)part_ws;
   if (c.plan || !c.ok()) return;
   set_smem(k_panel_rev, PR_SMEM);
@@ -696,9 +699,6 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     int j, w;
     block_range(n, nb, true, qb, j, w);
     const int k = j + w, p = n - k;
-    const Opnd Dinv_q = ws_opnd(Dinv + int64_t(qb) * nb * nb, int64_t(nblk) * nb * nb, nb);
-    const Opnd S = ws_opnd(Sall + int64_t(qb) * (LL_BM + 4) * LL_BM, s_stride, LL_BM + 4);
-    const Opnd W = sub(A, k, j);
     if (p > 0) {
       LLParams lp;
       lp.A = A;
@@ -716,27 +716,31 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       }
       k_symm_ll<<<lp.G, LL_THREADS, LL_SMEM, c.st>>>(lp, w < nb ? tm_short : tm);
       c.launched();
-      // Cbar <- Cbar D^{-1};  Dbar <- Dbar - tril(Cbar^T C)   (one cooperative kernel)
-      PanelParams pp;
-      pp.A = A;
-      pp.L = L;
-      pp.Dinv = Dinv + int64_t(qb) * nb * nb;
-      pp.dstride = int64_t(nblk) * nb * nb;
-      pp.dld = nb;
-      pp.n = n, pp.j = j, pp.w = w, pp.k = k;
-      pp.tiles = p / LL_BM;
-      pp.batch = batch;
-      pp.part = prpart;
-      const int64_t units = batch * pp.tiles;
-      const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs (phase 2)
-      (void)units;
-      void* args[] = {&pp};
-      c.pre(CD_PROF_PANEL, double(p) * w * (w + 1) * 2.0 * double(batch));
-      c.err = note_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_panel_rev), dim3(grid),
-                                                    dim3(PR_THREADS), args, PR_SMEM, c.st));
-      c.launched();
     }
-    run_sweep_small<double>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, qb > 0 ? S : null_opnd(), nullptr);
+    // Cbar <- Cbar D^{-1};  Dbar <- Dbar - tril(Cbar^T C);  Dbar <- chol_unblocked_rev(D, Dbar)
+    // (Eq. 10) + S -- one cooperative kernel
+    PanelParams pp;
+    pp.A = A;
+    pp.L = L;
+    pp.Dinv = Dinv + int64_t(qb) * nb * nb;
+    pp.dstride = int64_t(nblk) * nb * nb;
+    pp.dld = nb;
+    pp.n = n, pp.j = j, pp.w = w, pp.k = k;
+    pp.tiles = p / LL_BM;
+    pp.batch = batch;
+    pp.part = prpart;
+    pp.Pws = Pws;
+    pp.Zws = Zws;
+    pp.S = qb > 0 ? Sall + int64_t(qb) * (LL_BM + 4) * LL_BM : nullptr;
+    pp.s_ld = LL_BM + 4;
+    pp.s_stride = s_stride;
+    const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs
+    void* args[] = {&pp};
+    const double wf = w;
+    c.pre(CD_PROF_PANEL, (double(p) * w * (w + 1) * 2.0 + (4 * wf * wf * wf + 3 * wf * wf + 11 * wf) / 6) * double(batch));
+    c.err = note_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_panel_rev), dim3(grid),
+                                                  dim3(PR_THREADS), args, PR_SMEM, c.st));
+    c.launched();
   }
   if (info && c.ok()) {
     c.pre(CD_PROF_OTHER, 0.0);

@@ -12,9 +12,12 @@
 //            warp's columns are skipped), stored in place and kept in shared memory;
 //            P_t = tril(W^T C_t) (warps above the diagonal skip), stored to slot t;
 //   grid sync (cooperative launch: all CTAs co-resident);
-//   phase 2  Dbar -= sum_t P_t over the lower triangle, four threads per element with a
-//            fixed summation tree (bitwise deterministic).
-// Replaces two split-K GEMM launches and their reduction launches on the critical path.
+//   phase 2  Dbar -= sum_t P_t over the lower triangle, eight lanes per element with a
+//            fixed summation tree (bitwise deterministic);
+//   phase 3  the diagonal block Dbar <- chol_unblocked_rev(D, Dbar) by Eq. 10, three
+//            32x32-tiled products over the grid (see below), also emitting S = Dbar + Dbar^T.
+// Replaces two split-K GEMM launches, their reduction launches and the one-CTA diagonal
+// sweep on the critical path.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -44,7 +47,45 @@ struct PanelParams {
   int tiles;         // (n - k) / 128 per matrix
   int64_t batch;
   double* part;      // [batch * tiles][128 * 128] slots
+  // phase 3 (diagonal block by Eq. 10): scratch P, Z (dense 128 x 128 per batch entry) and
+  // the S output (dense, ld s_ld, batch stride s_stride; nullptr = not needed)
+  double* Pws;
+  double* Zws;
+  double* S;
+  int s_ld;
+  int64_t s_stride;
 };
+
+// One 32 x 32 output tile of C = A B (K = 128, zero-padded) on a CTA: A(m, k) and B(k, n)
+// are gathered by the fill functors into shared memory as As[m][k], Bs[n][k] (pitch 132:
+// conflict-free DMMA fragment loads); each warp owns two 8 x 8 sub-tiles; the epilogue
+// functor gets (row m, column n, value).
+template <class FA, class FB, class EP>
+__device__ __forceinline__ void pr_tile32(double* sm, FA fa, FB fb, EP ep) {
+  constexpr int P = 132;
+  double* As = sm;
+  double* Bs = sm + 32 * P;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  __syncthreads();  // smem reuse
+  for (int e = tid; e < 32 * 128; e += PR_THREADS) {
+    const int k = e & 127, m = e >> 7;
+    As[m * P + k] = fa(m, k);
+    Bs[m * P + k] = fb(k, m);
+  }
+  __syncthreads();
+  const int mt = warp >> 1, nt0 = (warp & 1) * 2;  // sub-tiles (mt, nt0) and (mt, nt0 + 1)
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 8
+  for (int kq = 0; kq < 32; ++kq) {
+    const double a = As[(8 * mt + g) * P + 4 * kq + t];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) dmma884(c[u][0], c[u][1], a, Bs[(8 * (nt0 + u) + g) * P + 4 * kq + t]);
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) ep(8 * mt + g, 8 * (nt0 + u) + 2 * t + e, c[u][e]);
+}
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
   unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -243,6 +284,87 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
       double* D = optr_w<double>(p.A, b) + (p.j + a) + int64_t(p.j + c) * p.A.ld;
       *D -= s;
     }
+  }
+
+  // ---------------- phase 3: Dbar <- chol_unblocked_rev(D, Dbar) by Eq. 10 ----------------
+  // The paper's own blocked implementation updates diagonal blocks with Eq. 10
+  // (Eq. 10 = PAPER.md:248-256):
+  //   P = Phi(D^T Dbar),  Y = D^{-T} (P + P^T) D^{-1},  tril(Dbar) = Phi(Y),  S = Y (= Dbar + Dbar^T)
+  // as three 128 x 128 products in 32 x 32 tiles over the grid (grid syncs between them).
+  // D^{-1} is the block inverse k_trinv already made for the panel solve.
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  const int64_t u3 = p.batch * 16;
+  // 3a: P = Phi(D^T Dbar)  (D, Dbar read as lower triangles)
+  for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
+    const int64_t b = u >> 4;
+    const int ti = int(u & 15) >> 2, tj = int(u & 3);
+    const double* Lb = optr<double>(p.L, b) + p.j + int64_t(p.j) * p.L.ld;
+    const double* Ab = optr<double>(p.A, b) + p.j + int64_t(p.j) * p.A.ld;
+    double* Pb = p.Pws + b * 128 * 128;
+    const int a0 = 32 * ti, c0 = 32 * tj;
+    pr_tile32(
+        sm,
+        [&](int m, int k) {  // A(m, k) = D(k, a0 + m)
+          const int a = a0 + m;
+          return (k < w && a < w && k >= a) ? Lb[k + int64_t(a) * p.L.ld] : 0.0;
+        },
+        [&](int k, int n) {  // B(k, n) = Dbar(k, c0 + n)
+          const int cc = c0 + n;
+          return (k < w && cc < w && k >= cc) ? Ab[k + int64_t(cc) * p.A.ld] : 0.0;
+        },
+        [&](int m, int n, double v) {
+          const int a = a0 + m, cc = c0 + n;
+          Pb[a + cc * 128] = a > cc ? v : (a == cc ? 0.5 * v : 0.0);
+        });
+  }
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  // 3b: Z = (P + P^T) D^{-1}
+  for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
+    const int64_t b = u >> 4;
+    const int ti = int(u & 15) >> 2, tj = int(u & 3);
+    const double* Pb = p.Pws + b * 128 * 128;
+    const double* Di = p.Dinv + b * p.dstride;
+    double* Zb = p.Zws + b * 128 * 128;
+    const int a0 = 32 * ti, c0 = 32 * tj;
+    pr_tile32(
+        sm, [&](int m, int k) { return __ldcg(Pb + (a0 + m) + k * 128) + __ldcg(Pb + k + (a0 + m) * 128); },
+        [&](int k, int n) {
+          const int cc = c0 + n;
+          return (k < w && cc < w) ? Di[k + int64_t(cc) * p.dld] : 0.0;
+        },
+        [&](int m, int n, double v) { Zb[(a0 + m) + (c0 + n) * 128] = v; });
+  }
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  // 3c: Y = D^{-T} Z (lower tiles);  tril(Dbar) = Phi(Y);  S = Y mirrored from its lower triangle
+  for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
+    const int64_t b = u >> 4;
+    const int ti = int(u & 15) >> 2, tj = int(u & 3);
+    if (ti < tj) continue;  // uniform per CTA
+    const double* Di = p.Dinv + b * p.dstride;
+    const double* Zb = p.Zws + b * 128 * 128;
+    double* Ab = optr_w<double>(p.A, b) + p.j + int64_t(p.j) * p.A.ld;
+    double* Sb = p.S ? p.S + b * p.s_stride : nullptr;
+    const int a0 = 32 * ti, c0 = 32 * tj;
+    pr_tile32(
+        sm,
+        [&](int m, int k) {  // A(m, k) = Dinv(k, a0 + m)
+          const int a = a0 + m;
+          return (k < w && a < w) ? Di[k + int64_t(a) * p.dld] : 0.0;
+        },
+        [&](int k, int n) { return __ldcg(Zb + k + (c0 + n) * 128); },
+        [&](int m, int n, double v) {
+          const int a = a0 + m, cc = c0 + n;
+          if (a < w && cc < w && a >= cc) {
+            Ab[a + int64_t(cc) * p.A.ld] = a == cc ? 0.5 * v : v;
+            if (Sb) {
+              Sb[a + int64_t(cc) * p.s_ld] = v;
+              Sb[cc + int64_t(a) * p.s_ld] = v;
+            }
+          }
+        });
   }
 }
 
