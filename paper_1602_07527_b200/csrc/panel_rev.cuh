@@ -56,10 +56,16 @@ struct PanelParams {
   int64_t s_stride;
 };
 
-// One 32 x 32 output tile of C = A B (K = 128, zero-padded) on a CTA: A(m, k) and B(k, n)
-// are gathered by the fill functors into shared memory as As[m][k], Bs[n][k] (pitch 132:
-// conflict-free DMMA fragment loads); each warp owns two 8 x 8 sub-tiles; the epilogue
-// functor gets (row m, column n, value).
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(valid ? 8 : 0));
+}
+
+// One 32 x 32 output tile of C = A B (K = 128, zero-padded) on a CTA.  The source functors
+// return a global pointer to A(m, k) / B(k, n), or nullptr for a zero; every element is
+// staged by an 8-byte cp.async (all in flight at once) into shared memory as As[m][k],
+// Bs[n][k] (pitch 132: conflict-free DMMA fragment loads).  Each warp owns two 8 x 8
+// sub-tiles; the epilogue functor gets (row m, column n, value).
 template <class FA, class FB, class EP>
 __device__ __forceinline__ void pr_tile32(double* sm, FA fa, FB fb, EP ep) {
   constexpr int P = 132;
@@ -69,9 +75,12 @@ __device__ __forceinline__ void pr_tile32(double* sm, FA fa, FB fb, EP ep) {
   __syncthreads();  // smem reuse
   for (int e = tid; e < 32 * 128; e += PR_THREADS) {
     const int k = e & 127, m = e >> 7;
-    As[m * P + k] = fa(m, k);
-    Bs[m * P + k] = fb(k, m);
+    const double* pa = fa(m, k);
+    const double* pb = fb(k, m);
+    cp_async8(As + m * P + k, pa ? pa : As, pa != nullptr);
+    cp_async8(Bs + m * P + k, pb ? pb : Bs, pb != nullptr);
   }
+  cp_async_wait_all();
   __syncthreads();
   const int mt = warp >> 1, nt0 = (warp & 1) * 2;  // sub-tiles (mt, nt0) and (mt, nt0 + 1)
   double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -85,11 +94,6 @@ __device__ __forceinline__ void pr_tile32(double* sm, FA fa, FB fb, EP ep) {
   for (int u = 0; u < 2; ++u)
 #pragma unroll
     for (int e = 0; e < 2; ++e) ep(8 * mt + g, 8 * (nt0 + u) + 2 * t + e, c[u][e]);
-}
-
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
-  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(valid ? 8 : 0));
 }
 
 __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p) {
@@ -266,17 +270,21 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
       while (c + 1 < w && (c + 1) * w - (c + 1) * c / 2 <= rem) ++c;
       a = c + (rem - (c * w - c * (c - 1) / 2));
     }
-    double s0 = 0.0, s1 = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (on) {
       const double* pb = p.part + b * p.tiles * int64_t(128 * 128) + a + c * 128;
+      constexpr int64_t TS = 128 * 128;
       int tl = q;
-      for (; tl + 8 < p.tiles; tl += 16) {
-        s0 += __ldcg(pb + int64_t(tl) * 128 * 128);
-        s1 += __ldcg(pb + int64_t(tl + 8) * 128 * 128);
+      for (; tl + 24 < p.tiles; tl += 32) {  // four independent loads in flight per lane
+        const double x0 = __ldcg(pb + tl * TS), x1 = __ldcg(pb + (tl + 8) * TS);
+        const double x2 = __ldcg(pb + (tl + 16) * TS), x3 = __ldcg(pb + (tl + 24) * TS);
+        s0 += x0, s1 += x1, s2 += x2, s3 += x3;
       }
-      if (tl < p.tiles) s0 += __ldcg(pb + int64_t(tl) * 128 * 128);
+      if (tl < p.tiles) s0 += __ldcg(pb + tl * TS);
+      if (tl + 8 < p.tiles) s1 += __ldcg(pb + (tl + 8) * TS);
+      if (tl + 16 < p.tiles) s2 += __ldcg(pb + (tl + 16) * TS);
     }
-    double s = s0 + s1;
+    double s = (s0 + s1) + (s2 + s3);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
@@ -295,44 +303,54 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   __threadfence();
   cooperative_groups::this_grid().sync();
   const int64_t u3 = p.batch * 16;
-  // 3a: P = Phi(D^T Dbar)  (D, Dbar read as lower triangles)
+  // 3a (lower tiles): X = P + P^T, P = Phi(D^T Dbar), written symmetric (D, Dbar read as
+  // lower triangles; X(a, a) = (D^T Dbar)(a, a), X(a, c) = X(c, a) = P(a, c) for a > c)
   for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
     const int64_t b = u >> 4;
     const int ti = int(u & 15) >> 2, tj = int(u & 3);
+    if (ti < tj) continue;  // uniform per CTA
     const double* Lb = optr<double>(p.L, b) + p.j + int64_t(p.j) * p.L.ld;
     const double* Ab = optr<double>(p.A, b) + p.j + int64_t(p.j) * p.A.ld;
-    double* Pb = p.Pws + b * 128 * 128;
+    double* Xb = p.Pws + b * 128 * 128;
     const int a0 = 32 * ti, c0 = 32 * tj;
     pr_tile32(
         sm,
-        [&](int m, int k) {  // A(m, k) = D(k, a0 + m)
+        [&](int m, int k) -> const double* {  // A(m, k) = D(k, a0 + m)
           const int a = a0 + m;
-          return (k < w && a < w && k >= a) ? Lb[k + int64_t(a) * p.L.ld] : 0.0;
+          return (k < w && a < w && k >= a) ? Lb + k + int64_t(a) * p.L.ld : nullptr;
         },
-        [&](int k, int n) {  // B(k, n) = Dbar(k, c0 + n)
+        [&](int k, int n) -> const double* {  // B(k, n) = Dbar(k, c0 + n)
           const int cc = c0 + n;
-          return (k < w && cc < w && k >= cc) ? Ab[k + int64_t(cc) * p.A.ld] : 0.0;
+          return (k < w && cc < w && k >= cc) ? Ab + k + int64_t(cc) * p.A.ld : nullptr;
         },
         [&](int m, int n, double v) {
           const int a = a0 + m, cc = c0 + n;
-          Pb[a + cc * 128] = a > cc ? v : (a == cc ? 0.5 * v : 0.0);
+          if (a > cc) {
+            Xb[a + cc * 128] = v;
+            Xb[cc + a * 128] = v;
+          } else if (a == cc) {
+            Xb[a + cc * 128] = v;
+          }
         });
   }
   __threadfence();
   cooperative_groups::this_grid().sync();
-  // 3b: Z = (P + P^T) D^{-1}
+  // 3b: Z = X D^{-1}   (A(m, k) = X(a0 + m, k) = X(k, a0 + m): a contiguous column)
   for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
     const int64_t b = u >> 4;
     const int ti = int(u & 15) >> 2, tj = int(u & 3);
-    const double* Pb = p.Pws + b * 128 * 128;
+    const double* Xb = p.Pws + b * 128 * 128;
     const double* Di = p.Dinv + b * p.dstride;
     double* Zb = p.Zws + b * 128 * 128;
     const int a0 = 32 * ti, c0 = 32 * tj;
     pr_tile32(
-        sm, [&](int m, int k) { return __ldcg(Pb + (a0 + m) + k * 128) + __ldcg(Pb + k + (a0 + m) * 128); },
-        [&](int k, int n) {
+        sm,
+        [&](int m, int k) -> const double* {
+          return (k < w && a0 + m < w) ? Xb + k + (a0 + m) * 128 : nullptr;
+        },
+        [&](int k, int n) -> const double* {
           const int cc = c0 + n;
-          return (k < w && cc < w) ? Di[k + int64_t(cc) * p.dld] : 0.0;
+          return (k < w && cc < w) ? Di + k + int64_t(cc) * p.dld : nullptr;
         },
         [&](int m, int n, double v) { Zb[(a0 + m) + (c0 + n) * 128] = v; });
   }
@@ -350,11 +368,11 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
     const int a0 = 32 * ti, c0 = 32 * tj;
     pr_tile32(
         sm,
-        [&](int m, int k) {  // A(m, k) = Dinv(k, a0 + m)
+        [&](int m, int k) -> const double* {  // A(m, k) = Dinv(k, a0 + m)
           const int a = a0 + m;
-          return (k < w && a < w) ? Di[k + int64_t(a) * p.dld] : 0.0;
+          return (k < w && a < w) ? Di + k + int64_t(a) * p.dld : nullptr;
         },
-        [&](int k, int n) { return __ldcg(Zb + k + (c0 + n) * 128); },
+        [&](int k, int n) -> const double* { return (k < w && c0 + n < w) ? Zb + k + (c0 + n) * 128 : nullptr; },
         [&](int m, int n, double v) {
           const int a = a0 + m, cc = c0 + n;
           if (a < w && cc < w && a >= cc) {
