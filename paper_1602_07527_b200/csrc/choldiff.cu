@@ -639,6 +639,7 @@ static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, 
 //                                               S = Dbar + Dbar^T kept per block for later M tiles
 // Requires fp64, nb = 128 and TMA-describable Abar / L (16-byte aligned, even ld).
 static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
+static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DEBUG_PANEL_SKIP")) : 0;
 
 static int panel_occupancy() {
   static int occ = 0;
@@ -734,6 +735,7 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pp.S = qb > 0 ? Sall + int64_t(qb) * (LL_BM + 4) * LL_BM : nullptr;
     pp.s_ld = LL_BM + 4;
     pp.s_stride = s_stride;
+    pp.dbg_skip = g_dbg_panel_skip;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs
     void* args[] = {&pp};
     const double wf = w;

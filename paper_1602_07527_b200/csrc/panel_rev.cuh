@@ -54,6 +54,7 @@ struct PanelParams {
   double* S;
   int s_ld;
   int64_t s_stride;
+  int dbg_skip;  // measurement only (CD_DEBUG_PANEL_SKIP): bit i skips phase i+1; results wrong
 };
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   const int w = p.w;
   const int64_t units = p.batch * p.tiles;
 
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+  for (int64_t u = blockIdx.x; u < units && !(p.dbg_skip & 1); u += gridDim.x) {
     const int64_t b = u / p.tiles;
     const int tl = int(u - b * p.tiles);
     const int r0 = p.k + 128 * tl;
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   const int64_t ntri = int64_t(w) * (w + 1) / 2;
   const int64_t nel = ntri * p.batch;  // lower-triangle entries (a >= c), column-packed
   const int q = lane & 7;
-  for (int64_t wb = gw * 4; wb < nel; wb += nwarps * 4) {
+  for (int64_t wb = gw * 4; wb < nel && !(p.dbg_skip & 2); wb += nwarps * 4) {
     const int64_t el = wb + (lane >> 3);
     const bool on = el < nel;
     int64_t b = 0;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   // D^{-1} is the block inverse k_trinv already made for the panel solve.
   __threadfence();
   cooperative_groups::this_grid().sync();
-  const int64_t u3 = p.batch * 16;
+  const int64_t u3 = (p.dbg_skip & 4) ? 0 : p.batch * 16;
   // 3a (lower tiles): X = P + P^T, P = Phi(D^T Dbar), written symmetric (D, Dbar read as
   // lower triangles; X(a, a) = (D^T Dbar)(a, a), X(a, c) = X(c, a) = P(a, c) for a > c)
   for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
