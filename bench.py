@@ -40,6 +40,7 @@ sys.path.insert(0, ROOT)
 METRIC = "chol_rev GFLOP/s (fp64, N=16384) and batched matrices/s; % of roofline"
 FP64_PEAK_TFLOPS = 37.0     # measured DMMA issue-rate peak (tools/microbench_fp64.cu, profiles/r01_microbench_fp64.txt)
 CUBLAS_DGEMM_TFLOPS = 35.5  # measured torch.matmul fp64 8192^3 (profiles/r01_torch_peaks.json), context only
+TF32_PEAK_TFLOPS = 1638.4 / 2  # MEASURED_PEAKS bf16 dense x the guide's nominal tf32:bf16 ratio (1:2)
 
 
 def rev_flops(n: int) -> int:
@@ -510,9 +511,18 @@ def bench_small_configs(args, dist: Dist):
         "workload": f"configs[3]: fp32 rev + fwd, {total} x N={n}, sharded by matrix over {P} GPU(s)",
         "ms_per_step": round(t, 3), "matrices_per_s": round(total / (t * 1e-3), 1),
         "gflops": round(fl / (t * 1e-3) / 1e9, 1),
-        "roofline": {"bound": "fp32 SIMT (FFMA) in round 1", "peak_tflops": 74.4,
-                     "frac": round(fl / (t * 1e-3) / 1e12 / 74.4, 4),
-                     "peak_source": "nominal 148 SM x 128 FFMA/clk x 2 x 1.965 GHz (cuBLAS SGEMM measured 64.0)"}}
+        # engines: tcgen05 kind::tf32 GEMMs + fp64-DMMA on-chip diagonal blocks.  Roofline =
+        # max(bytes / HBM, flops / tf32 peak); the HBM term wins: 5 T(512) fp32 triangles per
+        # matrix moved once (L shared by rev and fwd), 0.41 ms for the batch
+        "roofline": {"bound": "hbm", "unit": "GB/s",
+                     "algorithmic_bytes_per_matrix": 5 * (n * (n + 1) // 2) * 4,
+                     "achieved": round(5 * (n * (n + 1) // 2) * 4 * total / P / (t * 1e-3) / 1e9, 1),
+                     "peak": measured_peaks().get("hbm_gbs", 6536.0),
+                     "frac": round(5 * (n * (n + 1) // 2) * 4 * total / P / (t * 1e-3) / 1e9
+                                   / measured_peaks().get("hbm_gbs", 6536.0), 4),
+                     "compute_floor_ms": round(fl / P / TF32_PEAK_TFLOPS / 1e9, 3),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs; tf32 peak = measured bf16 dense x 1/2 "
+                                    "(profiling guide's nominal ratio)"}}
     return out
 
 

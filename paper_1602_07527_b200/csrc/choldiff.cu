@@ -810,8 +810,10 @@ struct Call {
 };
 
 static int default_nb(cd_dtype dt, int64_t n) {
-  (void)dt;
-  (void)n;
+  // fp64: 128 (the left-looking schedule's tile).  fp32 mid-size (batched tf32 path):
+  // 64 -- the on-chip diagonal-block kernels then fit several CTAs per SM, which beats
+  // the extra GEMM launches (1024 x 512 batched: rev 4.28 -> 3.39 ms, fwd 4.10 -> 2.83 ms)
+  if (dt == CD_F32 && n <= 1024) return 64;
   return 128;
 }
 
