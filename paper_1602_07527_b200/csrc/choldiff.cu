@@ -35,6 +35,8 @@
 #include "sweep_dmma_cta.cuh"
 #include "symm_ll.cuh"
 #include "panel_rev.cuh"
+#include "panel_fwd.cuh"
+#include "gemm_fwd_sk.cuh"
 
 namespace cd {
 
@@ -799,6 +801,109 @@ static void blocked_fwd(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
   }
 }
 
+// ------------------------------------------------------------------ blocked forward, fused panels
+// chol_blocked_fwd for fp64, nb = 128, TMA-describable operands, as two
+// launches per panel J = [j, k):
+//   k_panel_fwd (cooperative): [previous panel's Cdot <- W D^{-T}], Ddot -= tril(Rdot R^T +
+//       R Rdot^T) (K-chunk partials + deterministic reduction), Ddot <- D Phi(D^{-1} Ddot D^{-T})
+//       (Eq. 8) + the clean copy Dc
+//   k_fwd_sk (stream-K):   W = Cdot - [Bdot B C] [R Rdot Dc]^T, in place
+// The last panel has no rows below it, so no W D^{-T} is left pending.
+static int panel_fwd_occupancy() {
+  static int occ = 0;
+  if (!occ) {
+    set_smem(k_panel_fwd, PR_SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_panel_fwd, PR_THREADS, PR_SMEM) != cudaSuccess || occ < 1)
+      occ = 1;
+  }
+  return occ;
+}
+
+static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info) {
+  const int nblk = nblocks(n, nb);
+  double* Dinv = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * nb * nb));
+  double* part = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
+  double* Yws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
+  double* Fws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
+  double* Dc = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 132 * 128));
+  double* skpart = static_cast<double*>(c.take(sizeof(double) * size_t(c.sms) * 2 * LL_TILE));
+  int* cnt = static_cast<int*>(c.take(sizeof(int) * size_t(batch) * nblk));
+  if (c.plan || !c.ok()) return;
+  FSMaps tm;
+  memset(&tm, 0, sizeof(tm));
+  tm.batched = batch > 1 ? 1 : 0;
+  {
+    int sh = 0;
+    const double* Ab = static_cast<const double*>(A.base) + A.off;
+    const double* Lb = static_cast<const double*>(L.base) + L.off;
+    const bool ok = make_tmap(&tm.adot, &sh, Ab, n, n, A.ld, A.stride, batch, FS_PITCH, LL_BK) &&
+                    make_tmap(&tm.l, &sh, Lb, n, n, L.ld, L.stride, batch, FS_PITCH, LL_BK) &&
+                    make_tmap(&tm.dc, &sh, Dc, 132, 128, 132, 132 * 128, batch, FS_PITCH, LL_BK);
+    if (!ok) {
+      c.err = CD_ERR_CUDA;
+      snprintf(g_cuda_err, sizeof(g_cuda_err), "cuTensorMapEncodeTiled failed for the forward sweep");
+      return;
+    }
+  }
+  c.err = note_cuda(cudaMemsetAsync(cnt, 0, sizeof(int) * size_t(batch) * nblk, c.st));
+  set_smem(k_fwd_sk, FS_SMEM);
+  set_smem(k_panel_fwd, PR_SMEM);
+  run_trinv<double>(c, n, nb, false, batch, L, Dinv);
+  int j_prev = 0, k_prev = 0, p_prev = 0;
+  for (int qb = 0; qb < nblk && c.ok(); ++qb) {
+    int j, w;
+    block_range(n, nb, false, qb, j, w);
+    const int k = j + w, p = n - k, q = j;
+    PanelFwdParams pf;
+    pf.A = A;
+    pf.L = L;
+    pf.Dinv = Dinv + int64_t(qb) * nb * nb;
+    pf.Dinv_prev = (qb > 0 && p_prev > 0) ? Dinv + int64_t(qb - 1) * nb * nb : nullptr;
+    pf.dstride = int64_t(nblk) * nb * nb;
+    pf.dld = nb;
+    pf.n = n, pf.j = j, pf.w = w;
+    pf.j_prev = j_prev, pf.k_prev = k_prev, pf.tiles_prev = (p_prev + 127) / 128;
+    pf.kchunks = q / 128;
+    pf.batch = batch;
+    pf.part = part;
+    pf.Yws = Yws;
+    pf.Fws = Fws;
+    pf.Dc = Dc;
+    const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
+    void* args[] = {&pf};
+    const double wf = w;
+    c.pre(CD_PROF_PANEL, (double(p_prev) * 128 * 129 + 2.0 * wf * (wf + 1) * q +
+                          (4 * wf * wf * wf + 3 * wf * wf + 5 * wf) / 6) * double(batch));
+    c.err = note_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_panel_fwd), dim3(grid),
+                                                  dim3(PR_THREADS), args, PR_SMEM, c.st));
+    c.launched();
+    if (p > 0 && c.ok()) {
+      FSParams fp;
+      fp.A = A;
+      fp.n = n, fp.k = k, fp.j = j, fp.w = w, fp.q = q;
+      fp.m = (p + 127) / 128;
+      fp.KT = (2 * q + w + LL_BK - 1) / LL_BK;
+      fp.total = batch * int64_t(fp.m) * fp.KT;
+      if (fp.total >= (int64_t(1) << 31) || w != 128) {
+        c.err = CD_ERR_UNSUPPORTED;
+        return;
+      }
+      fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
+      fp.part = skpart;
+      fp.cnt = cnt;
+      c.pre(CD_PROF_SYMM, 2.0 * double(p) * w * (2.0 * q + w) * double(batch));
+      k_fwd_sk<<<fp.G, LL_THREADS, FS_SMEM, c.st>>>(fp, tm);
+      c.launched();
+    }
+    j_prev = j, k_prev = k, p_prev = p;
+  }
+  if (info && c.ok()) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_diag_info<double><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
+    c.launched();
+  }
+}
+
 // ------------------------------------------------------------------ top-level
 struct Call {
   cd_op op;
@@ -855,7 +960,22 @@ static void drive(Ctx& c, const Call& k) {
     }
     c.off = std::max(c.off, o_ll);
   } else {
-    blocked_fwd<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+    // fused-panel forward schedule (fp64, nb = 128, TMA-describable operands); the plan sizes
+    // the workspace for both schedules (see above)
+    const bool fl_shape = k.dt == CD_F64 && nb == LL_BM && !g_no_ll && !g_tma_disabled && !k.L.arr && !k.A.arr;
+    const bool fl = fl_shape && (c.plan || ((reinterpret_cast<uintptr_t>(static_cast<const double*>(k.A.base) + k.A.off) % 16) == 0 &&
+                                            (reinterpret_cast<uintptr_t>(static_cast<const double*>(k.L.base) + k.L.off) % 16) == 0 &&
+                                            k.A.ld % 2 == 0 && k.L.ld % 2 == 0 &&
+                                            (k.batch == 1 || (k.A.stride % 2 == 0 && k.L.stride % 2 == 0))));
+    const size_t o0 = c.off;
+    size_t o_fl = o0;
+    if (fl) {
+      blocked_fwd_ll(c, n, nb, k.batch, k.L, k.A, k.info);
+      o_fl = c.off;
+      c.off = o0;
+    }
+    if (!fl || c.plan) blocked_fwd<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
+    c.off = std::max(c.off, o_fl);
   }
   if (k.op == CD_OP_REV && k.o.out_mode != CD_OUT_TRIL && !c.plan && c.ok()) {
     c.pre(CD_PROF_OTHER, 0.0);

@@ -1,0 +1,260 @@
+// panel_fwd.cuh -- the per-panel steps of the blocked FORWARD sweep as ONE cooperative
+// kernel (fp64, DMMA), the forward counterpart of panel_rev.cuh.  For panel J = [j, k)
+// (q = j columns to its left):
+//
+//   phase 0  the previous panel's  Cdot <- W D^{-T}   (W is left in place by
+//            k_fwd_sk), 32 x 32 output tiles staged and copied back after a grid sync;
+//   phase 1  Ddot <- Ddot - tril(Rdot R^T + R Rdot^T): one CTA per (128-wide
+//            K chunk, lower 32 x 32 tile) computes a partial (both products);
+//   phase 2  deterministic grid reduction of the partials into Ddot;
+//   phase 3  the diagonal block by Eq. 8 (the paper names Eqs. 8/10 as
+//            the natural diagonal-block updates):
+//              Y = D^{-1} Ddot_sym,  F = Phi(Y D^{-T}),  Ldot_D = D F,
+//            Ldot_D written over tril(Ddot) and as the clean dense copy Dc (upper zero)
+//            that the next k_fwd_sk consumes (segment C Ddot^T).
+// Grid syncs separate the phases.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "panel_rev.cuh"  // PR_* constants, cp_async8, pr_tile32
+
+namespace cd {
+
+struct PanelFwdParams {
+  Opnd A, L;             // Adot and L (whole matrices)
+  const double* Dinv;    // this panel's D^{-1} (w x w, ld dld; batch stride dstride)
+  const double* Dinv_prev;  // the previous panel's (phase 0), or nullptr
+  int64_t dstride;
+  int dld;
+  int n, j, w;
+  int j_prev, k_prev, tiles_prev;  // phase 0: rows [k_prev, n) in ceil(.) 128-row tiles, cols [j_prev, j_prev+128)
+  int kchunks;           // phase 1: q / 128
+  int64_t batch;
+  double* part;          // [batch * kchunks][128 * 128] (phase 1); phase 0 staging [units][32 * 32]
+  double* Yws;           // dense 128 x 128 per batch entry
+  double* Fws;           // dense 128 x 128 per batch entry
+  double* Dc;            // dense, ld 132, batch stride 132 * 128
+};
+
+__global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParams p) {
+  extern __shared__ __align__(16) unsigned char smem_pf[];
+  double* sm = reinterpret_cast<double*>(smem_pf);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = p.w;
+  namespace cg = cooperative_groups;
+
+  // ---------------- phase 0: previous panel  Cdot <- W D_prev^{-T} ----------------
+  // 32 x 32 output tiles (16 per 128-row tile), so small panels still spread over the GPU
+  if (p.Dinv_prev) {
+    const int64_t units = p.batch * p.tiles_prev * 16;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int64_t bt = u >> 4;
+      const int64_t b = bt / p.tiles_prev;
+      const int tl = int(bt - b * p.tiles_prev);
+      const int ti = int(u & 15) >> 2, tj = int(u & 3);
+      const int r0 = p.k_prev + 128 * tl + 32 * ti, c0 = 32 * tj;
+      const double* Wt = optr<double>(p.A, b) + r0 + int64_t(p.j_prev) * p.A.ld;  // rows r0.., panel cols
+      const double* Di = p.Dinv_prev + b * p.dstride;
+      // write target: column-group tj of the same rows; the 4 column groups of a row group
+      // read all of W's columns, so results go to the Yws-like staging slot first
+      double* st = p.part + u * int64_t(32 * 32);
+      pr_tile32(
+          sm, [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.A.ld : nullptr; },
+          [&](int kk, int n) -> const double* {
+            const int cc = c0 + n;
+            return cc >= kk ? Di + cc + int64_t(kk) * p.dld : nullptr;  // D^{-T}(kk, cc) = Dinv(cc, kk)
+          },
+          [&](int m, int n, double v) { __stcg(st + m + n * 32, v); });
+    }
+    __threadfence();
+    cg::this_grid().sync();
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {  // copy the staged tiles back
+      const int64_t bt = u >> 4;
+      const int64_t b = bt / p.tiles_prev;
+      const int tl = int(bt - b * p.tiles_prev);
+      const int ti = int(u & 15) >> 2, tj = int(u & 3);
+      const int r0 = p.k_prev + 128 * tl + 32 * ti, c0 = 32 * tj;
+      double* Wt = optr_w<double>(p.A, b) + r0 + int64_t(p.j_prev + c0) * p.A.ld;
+      const double* st = p.part + u * int64_t(32 * 32);
+      for (int e = tid; e < 32 * 32; e += PR_THREADS) {
+        const int m = e & 31, n = e >> 5;
+        if (r0 + m < p.n) Wt[m + int64_t(n) * p.A.ld] = __ldcg(st + e);
+      }
+    }
+    __threadfence();
+    cg::this_grid().sync();
+  }
+
+  // ---------------- phase 1: partials of Rdot R^T + R Rdot^T ----------------
+  // unit = (128-wide K chunk, lower 32 x 32 tile of the w x w block): K = 256 (both products)
+  {
+    const int64_t units = p.batch * p.kchunks * 10;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int64_t bk = u / 10;
+      const int lt = int(u - bk * 10);
+      int ti = 0, tj = 0;  // lower tile lt -> (ti >= tj)
+      {
+        int r = lt;
+        while (r > ti) r -= ++ti;
+        tj = r;
+      }
+      const int64_t b = bk / p.kchunks;
+      const int kc0 = 128 * int(bk - b * p.kchunks);
+      const double* Ad = optr<double>(p.A, b) + p.j + int64_t(kc0) * p.A.ld;  // Rdot chunk, rows j..
+      const double* Lr = optr<double>(p.L, b) + p.j + int64_t(kc0) * p.L.ld;  // R chunk
+      const int a0 = 32 * ti, c0 = 32 * tj;
+      double* slot = p.part + bk * int64_t(128 * 128);
+      // kk < 128 -> Rdot(a, kk) R(c, kk); kk >= 128 -> R(a, kk') Rdot(c, kk')
+      pr_tile32k(
+          sm, 256,
+          [&](int m, int kk) -> const double* {
+            const int a = a0 + m;
+            if (a >= w) return nullptr;
+            return kk < 128 ? Ad + a + int64_t(kk) * p.A.ld : Lr + a + int64_t(kk - 128) * p.L.ld;
+          },
+          [&](int kk, int n) -> const double* {
+            const int cc = c0 + n;
+            if (cc >= w) return nullptr;
+            return kk < 128 ? Lr + cc + int64_t(kk) * p.L.ld : Ad + cc + int64_t(kk - 128) * p.A.ld;
+          },
+          [&](int m, int n, double v) {
+            const int a = a0 + m, cc = c0 + n;
+            if (a >= cc) __stcg(slot + a + cc * 128, v);
+          });
+    }
+  }
+  __threadfence();
+  cg::this_grid().sync();
+
+  // ---------------- phase 2: Ddot -= sum of the partials (lower triangle) ----------------
+  if (p.kchunks > 0) {
+    const int64_t nwarps = int64_t(gridDim.x) * (PR_THREADS / 32);
+    const int64_t gw = int64_t(blockIdx.x) * (PR_THREADS / 32) + warp;
+    const int64_t ntri = int64_t(w) * (w + 1) / 2;
+    const int64_t nel = ntri * p.batch;
+    const int q = lane & 7;
+    for (int64_t wb = gw * 4; wb < nel; wb += nwarps * 4) {
+      const int64_t el = wb + (lane >> 3);
+      const bool on = el < nel;
+      int64_t b = 0;
+      int a = 0, c = 0;
+      if (on) {
+        b = el / ntri;
+        const int rem = int(el - b * ntri);
+        const double tw = 2.0 * w + 1.0;
+        c = int((tw - sqrt(tw * tw - 8.0 * rem)) * 0.5);
+        c = max(0, min(c, w - 1));
+        while (c > 0 && c * w - c * (c - 1) / 2 > rem) --c;
+        while (c + 1 < w && (c + 1) * w - (c + 1) * c / 2 <= rem) ++c;
+        a = c + (rem - (c * w - c * (c - 1) / 2));
+      }
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (on) {
+        const double* pb = p.part + b * p.kchunks * int64_t(128 * 128) + a + c * 128;
+        constexpr int64_t TS = 128 * 128;
+        int tl = q;
+        for (; tl + 24 < p.kchunks; tl += 32) {
+          const double x0 = __ldcg(pb + tl * TS), x1 = __ldcg(pb + (tl + 8) * TS);
+          const double x2 = __ldcg(pb + (tl + 16) * TS), x3 = __ldcg(pb + (tl + 24) * TS);
+          s0 += x0, s1 += x1, s2 += x2, s3 += x3;
+        }
+        if (tl < p.kchunks) s0 += __ldcg(pb + tl * TS);
+        if (tl + 8 < p.kchunks) s1 += __ldcg(pb + (tl + 8) * TS);
+        if (tl + 16 < p.kchunks) s2 += __ldcg(pb + (tl + 16) * TS);
+      }
+      double s = (s0 + s1) + (s2 + s3);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (q == 0 && on) {
+        double* D = optr_w<double>(p.A, b) + (p.j + a) + int64_t(p.j + c) * p.A.ld;
+        *D -= s;
+      }
+    }
+    __threadfence();
+    cg::this_grid().sync();
+  }
+
+  // ---------------- phase 3: Ldot_D = D Phi(D^{-1} Ddot_sym D^{-T})  (Eq. 8) ----------------
+  const int64_t u3 = p.batch * 16;
+  // 3a: Y = D^{-1} X,  X(r, c) = Ddot(max, min)
+  for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
+    const int64_t b = u >> 4;
+    const int ti = int(u & 15) >> 2, tj = int(u & 3);
+    const double* Di = p.Dinv + b * p.dstride;
+    const double* Ab = optr<double>(p.A, b) + p.j + int64_t(p.j) * p.A.ld;
+    double* Yb = p.Yws + b * 128 * 128;
+    const int a0 = 32 * ti, c0 = 32 * tj;
+    pr_tile32(
+        sm,
+        [&](int m, int k) -> const double* {  // A(m, k) = Dinv(a0 + m, k)
+          const int a = a0 + m;
+          return (k < w && a < w && k <= a) ? Di + a + int64_t(k) * p.dld : nullptr;
+        },
+        [&](int k, int n) -> const double* {  // B(k, n) = X(k, c0 + n)
+          const int cc = c0 + n;
+          if (k >= w || cc >= w) return nullptr;
+          return k >= cc ? Ab + k + int64_t(cc) * p.A.ld : Ab + cc + int64_t(k) * p.A.ld;
+        },
+        [&](int m, int n, double v) { Yb[(a0 + m) + (c0 + n) * 128] = v; });
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  // 3b (lower tiles): F = Phi(Y D^{-T})
+  for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
+    const int64_t b = u >> 4;
+    const int ti = int(u & 15) >> 2, tj = int(u & 3);
+    if (ti < tj) continue;
+    const double* Di = p.Dinv + b * p.dstride;
+    const double* Yb = p.Yws + b * 128 * 128;
+    double* Fb = p.Fws + b * 128 * 128;
+    const int a0 = 32 * ti, c0 = 32 * tj;
+    pr_tile32(
+        sm,
+        [&](int m, int k) -> const double* { return (k < w && a0 + m < w) ? Yb + (a0 + m) + k * 128 : nullptr; },
+        [&](int k, int n) -> const double* {  // B(k, n) = Dinv(c0 + n, k)
+          const int cc = c0 + n;
+          return (k < w && cc < w && k <= cc) ? Di + cc + int64_t(k) * p.dld : nullptr;
+        },
+        [&](int m, int n, double v) {
+          const int a = a0 + m, cc = c0 + n;
+          Fb[a + cc * 128] = a > cc ? v : (a == cc ? 0.5 * v : 0.0);
+        });
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  // 3c (lower tiles): Ldot_D = D F  -> tril(Ddot) and Dc
+  for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
+    const int64_t b = u >> 4;
+    const int ti = int(u & 15) >> 2, tj = int(u & 3);
+    const double* Lb = optr<double>(p.L, b) + p.j + int64_t(p.j) * p.L.ld;
+    const double* Fb = p.Fws + b * 128 * 128;
+    double* Ab = optr_w<double>(p.A, b) + p.j + int64_t(p.j) * p.A.ld;
+    double* Dcb = p.Dc + b * int64_t(132 * 128);
+    const int a0 = 32 * ti, c0 = 32 * tj;
+    if (ti < tj) {  // upper tile of Dc: zero
+      for (int e = tid; e < 32 * 32; e += PR_THREADS) Dcb[(a0 + (e & 31)) + (c0 + (e >> 5)) * 132] = 0.0;
+      continue;
+    }
+    pr_tile32(
+        sm,
+        [&](int m, int k) -> const double* {  // A(m, k) = D(a0 + m, k)
+          const int a = a0 + m;
+          return (k < w && a < w && k <= a) ? Lb + a + int64_t(k) * p.L.ld : nullptr;
+        },
+        [&](int k, int n) -> const double* {  // B(k, n) = F(k, c0 + n), lower
+          const int cc = c0 + n;
+          return (k < w && cc < w && k >= cc) ? Fb + k + cc * 128 : nullptr;
+        },
+        [&](int m, int n, double v) {
+          const int a = a0 + m, cc = c0 + n;
+          const bool low = a >= cc && a < w && cc < w;
+          if (low) Ab[a + int64_t(cc) * p.A.ld] = v;
+          Dcb[a + cc * 132] = low ? v : 0.0;
+        });
+  }
+}
+
+}  // namespace cd

@@ -62,39 +62,47 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(valid ? 8 : 0));
 }
 
-// One 32 x 32 output tile of C = A B (K = 128, zero-padded) on a CTA.  The source functors
+// One 32 x 32 output tile of C = A B (K = 128, or any multiple of 128 for pr_tile32k,
+// zero-padded) on a CTA.  The source functors
 // return a global pointer to A(m, k) / B(k, n), or nullptr for a zero; every element is
 // staged by an 8-byte cp.async (all in flight at once) into shared memory as As[m][k],
 // Bs[n][k] (pitch 132: conflict-free DMMA fragment loads).  Each warp owns two 8 x 8
 // sub-tiles; the epilogue functor gets (row m, column n, value).
 template <class FA, class FB, class EP>
-__device__ __forceinline__ void pr_tile32(double* sm, FA fa, FB fb, EP ep) {
+__device__ __forceinline__ void pr_tile32k(double* sm, int K, FA fa, FB fb, EP ep) {
   constexpr int P = 132;
   double* As = sm;
   double* Bs = sm + 32 * P;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  __syncthreads();  // smem reuse
-  for (int e = tid; e < 32 * 128; e += PR_THREADS) {
-    const int k = e & 127, m = e >> 7;
-    const double* pa = fa(m, k);
-    const double* pb = fb(k, m);
-    cp_async8(As + m * P + k, pa ? pa : As, pa != nullptr);
-    cp_async8(Bs + m * P + k, pb ? pb : Bs, pb != nullptr);
-  }
-  cp_async_wait_all();
-  __syncthreads();
   const int mt = warp >> 1, nt0 = (warp & 1) * 2;  // sub-tiles (mt, nt0) and (mt, nt0 + 1)
   double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int kb = 0; kb < K; kb += 128) {
+    __syncthreads();  // smem reuse
+    for (int e = tid; e < 32 * 128; e += PR_THREADS) {
+      const int k = e & 127, m = e >> 7;
+      const double* pa = fa(m, kb + k);
+      const double* pb = fb(kb + k, m);
+      cp_async8(As + m * P + k, pa ? pa : As, pa != nullptr);
+      cp_async8(Bs + m * P + k, pb ? pb : Bs, pb != nullptr);
+    }
+    cp_async_wait_all();
+    __syncthreads();
 #pragma unroll 8
-  for (int kq = 0; kq < 32; ++kq) {
-    const double a = As[(8 * mt + g) * P + 4 * kq + t];
+    for (int kq = 0; kq < 32; ++kq) {
+      const double a = As[(8 * mt + g) * P + 4 * kq + t];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) dmma884(c[u][0], c[u][1], a, Bs[(8 * (nt0 + u) + g) * P + 4 * kq + t]);
+      for (int u = 0; u < 2; ++u) dmma884(c[u][0], c[u][1], a, Bs[(8 * (nt0 + u) + g) * P + 4 * kq + t]);
+    }
   }
 #pragma unroll
   for (int u = 0; u < 2; ++u)
 #pragma unroll
     for (int e = 0; e < 2; ++e) ep(8 * mt + g, 8 * (nt0 + u) + 2 * t + e, c[u][e]);
+}
+
+template <class FA, class FB, class EP>
+__device__ __forceinline__ void pr_tile32(double* sm, FA fa, FB fb, EP ep) {
+  pr_tile32k(sm, 128, fa, fb, ep);
 }
 
 __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p) {
