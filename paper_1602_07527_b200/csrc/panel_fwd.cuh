@@ -38,6 +38,62 @@ struct PanelFwdParams {
   double* Dc;            // dense, ld 132, batch stride 132 * 128
 };
 
+// acc (64 x 32 warp tiles of a 128 x 128 tile) += sum over K of A(m, kk) B(kk, c), K in
+// chunks of 16 (3-stage cp.async pipeline); fa / fb return the source pointer or nullptr
+// (zero).  skip(kc) (warp-uniform) drops a chunk for this warp.  Stage layout As[k][m],
+// Bs[k][c], pitch 132 (conflict-free fragments).  Used when a phase has enough 128-wide
+// units to fill the GPU (fewer operand re-reads than 32 x 32 tiles).
+template <class FA, class FB, class SK>
+__device__ __forceinline__ void pf_prod128(double* sm, int K, FA fa, FB fb, SK skip, double (&acc)[8][4][2]) {
+  constexpr int P = 132, STG = 2 * 16 * P;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3, g = lane >> 2, t = lane & 3;
+  const int nkc = (K + 15) / 16;
+  auto load = [&](int st, int kc) {
+    double* as = sm + st * STG;
+    double* bs = as + 16 * P;
+    for (int e = tid; e < 16 * 128; e += PR_THREADS) {
+      const int m = e & 127, kx = e >> 7;
+      const int kk = kc * 16 + kx;
+      const double* pa = kk < K ? fa(m, kk) : nullptr;
+      const double* pb = kk < K ? fb(kk, m) : nullptr;
+      cp_async8(as + kx * P + m, pa ? pa : as, pa != nullptr);
+      cp_async8(bs + kx * P + m, pb ? pb : bs, pb != nullptr);
+    }
+  };
+  __syncthreads();  // previous users of the stage buffers are done
+#pragma unroll 1
+  for (int s = 0; s < 2; ++s) {
+    if (s < nkc) load(s, s);
+    cp_async_commit();
+  }
+#pragma unroll 1
+  for (int kc = 0; kc < nkc; ++kc) {
+    cp_async_wait<1>();
+    __syncthreads();
+    if (kc + 2 < nkc) load((kc + 2) % 3, kc + 2);
+    cp_async_commit();
+    if (!skip(kc)) {
+      const double* as = sm + (kc % 3) * STG;
+      const double* bs = as + 16 * P;
+#pragma unroll
+      for (int kq = 0; kq < 4; ++kq) {
+        const int kx = kq * 4 + t;
+        double a[8], bb[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = as[kx * P + wm * 64 + i * 8 + g];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[kx * P + wn * 32 + jj * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
+      }
+    }
+  }
+  cp_async_wait_all();
+}
+
 __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParams p) {
   extern __shared__ __align__(16) unsigned char smem_pf[];
   double* sm = reinterpret_cast<double*>(smem_pf);
@@ -47,7 +103,41 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
 
   // ---------------- phase 0: previous panel  Cdot <- W D_prev^{-T} ----------------
   // 32 x 32 output tiles (16 per 128-row tile), so small panels still spread over the GPU
-  if (p.Dinv_prev) {
+  const bool big0 = p.batch * p.tiles_prev >= int64_t(gridDim.x) / 2;
+  if (p.Dinv_prev && big0) {  // one CTA per 128-row tile
+    const int lane_ = threadIdx.x & 31, wm = warp >> 2, wn = warp & 3, g = lane_ >> 2, t = lane_ & 3;
+    const int64_t units = p.batch * p.tiles_prev;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int64_t b = u / p.tiles_prev;
+      const int tl = int(u - b * p.tiles_prev);
+      const int r0 = p.k_prev + 128 * tl;
+      double* Wt = optr_w<double>(p.A, b) + r0 + int64_t(p.j_prev) * p.A.ld;
+      const double* Di = p.Dinv_prev + b * p.dstride;
+      double acc[8][4][2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+      pf_prod128(
+          sm, 128,
+          [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.A.ld : nullptr; },
+          [&](int kk, int c) -> const double* { return c >= kk ? Di + c + int64_t(kk) * p.dld : nullptr; },
+          [&](int kc) { return kc * 16 > wn * 32 + 31; },  // D^{-T}(kk, c) = 0 for kk > c
+          acc);
+      __syncthreads();  // every warp has read its W rows before any is overwritten
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = wm * 64 + i * 8 + g, c = wn * 32 + jj * 8 + 2 * t + e;
+            if (r0 + r < p.n) Wt[r + int64_t(c) * p.A.ld] = acc[i][jj][e];
+          }
+    }
+    __threadfence();
+    cg::this_grid().sync();
+  } else if (p.Dinv_prev) {
     const int64_t units = p.batch * p.tiles_prev * 16;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int64_t bt = u >> 4;
@@ -88,8 +178,46 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   }
 
   // ---------------- phase 1: partials of Rdot R^T + R Rdot^T ----------------
-  // unit = (128-wide K chunk, lower 32 x 32 tile of the w x w block): K = 256 (both products)
-  {
+  // unit = (128-wide K chunk, lower 32 x 32 tile of the w x w block): K = 256 (both
+  // products); with enough K chunks, one CTA per chunk computes the whole 128 x 128 block
+  const bool big1 = p.batch * p.kchunks >= int64_t(gridDim.x) / 2;
+  if (big1) {
+    const int lane_ = threadIdx.x & 31, wm = warp >> 2, wn = warp & 3, g = lane_ >> 2, t = lane_ & 3;
+    const int64_t units = p.batch * p.kchunks;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int64_t b = u / p.kchunks;
+      const int kc0 = 128 * int(u - b * p.kchunks);
+      const double* Ad = optr<double>(p.A, b) + p.j + int64_t(kc0) * p.A.ld;
+      const double* Lr = optr<double>(p.L, b) + p.j + int64_t(kc0) * p.L.ld;
+      double acc[8][4][2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+      pf_prod128(
+          sm, 256,
+          [&](int m, int kk) -> const double* {
+            if (m >= w) return nullptr;
+            return kk < 128 ? Ad + m + int64_t(kk) * p.A.ld : Lr + m + int64_t(kk - 128) * p.L.ld;
+          },
+          [&](int kk, int c) -> const double* {
+            if (c >= w) return nullptr;
+            return kk < 128 ? Lr + c + int64_t(kk) * p.L.ld : Ad + c + int64_t(kk - 128) * p.A.ld;
+          },
+          [&](int) { return wm * 64 + 63 < wn * 32; },  // warp tile entirely above the diagonal
+          acc);
+      double* slot = p.part + u * int64_t(128 * 128);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = wm * 64 + i * 8 + g, c = wn * 32 + jj * 8 + 2 * t + e;
+            if (r >= c) __stcg(slot + r + c * 128, acc[i][jj][e]);
+          }
+    }
+  } else {
     const int64_t units = p.batch * p.kchunks * 10;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int64_t bk = u / 10;
