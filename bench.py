@@ -282,6 +282,19 @@ def bench_single_rev(args, dist: Dist):
             out["roofline"]["hbm_peak_gbs"] = peaks.get("hbm_gbs")
     out["clocks"] = clk.summary()
 
+    # ---- the blocked forward sweep alongside, same N and L; Sigma_dot's
+    # lower triangle is an N(0,1) draw like L_bar's, so tril(L_bar) serves as its input
+    if args.fwd_steps > 0:
+        def fstep():
+            cd.chol_fwd(Ld, A, nb=nb)
+
+        fms = timed_steps(fstep, restore, args.fwd_steps, 1, dist, stream)
+        fw = dist.max(statistics.mean(fms))
+        out["fwd"] = {"workload": f"chol_fwd fp64 single matrix N={n} (same L), nb={nb}",
+                      "ms_per_step": round(fw, 3), "value": round(fwd_flops(n) / (fw * 1e-3) / 1e9, 2),
+                      "unit": "GFLOP/s", "frac_of_fp64_peak": round(fwd_flops(n) / (fw * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                      "steps": args.fwd_steps}
+
     # ---- e2e through the host-buffer C-ABI call
     if args.e2e_steps > 0:
         pin_L = torch.from_numpy(Lcm).pin_memory().transpose(0, 1)
@@ -585,6 +598,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--steps-batched", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--fwd-steps", type=int, default=2, help="timed chol_fwd steps at the same N (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-cols", type=int, default=1024)
     ap.add_argument("--no-cpu", action="store_true")

@@ -342,7 +342,10 @@ struct Gemm {
     }
     auto kern = k_gemm_tc32<A_, B_>;
     set_smem(kern, TC_SMEM);
-    kern<<<grid, TC_THREADS, TC_SMEM, c.st>>>(p, tm);
+    // persistent: a grid of (up to) 2 CTAs per SM loops over the units (TMEM: 2 x 256 columns)
+    const int64_t units = int64_t(grid.x) * grid.y * grid.z;
+    const unsigned g = unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(c.sms) * 2)));
+    kern<<<g, TCP_THREADS, TC_SMEM, c.st>>>(p, tm);
     c.launched();
     return true;
   }

@@ -28,16 +28,16 @@
 namespace cd {
 
 #ifndef CD_TC_STAGES
-#define CD_TC_STAGES 2
+#define CD_TC_STAGES 3
 #endif
 #ifndef CD_TC_MINB
-#define CD_TC_MINB 3
+#define CD_TC_MINB 2
 #endif
 constexpr int TC_STAGES = CD_TC_STAGES;
 constexpr int TC_THREADS = 128;
 constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32;
 constexpr uint32_t TC_STAGE_BYTES = (TC_BM + TC_BN) * TC_BK * 4;  // 32 KB
-constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + 1024 + 256;
+constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + 1024 + 256;  // + barriers, TMEM slot
 
 // shared-memory matrix descriptor; layout 2 = SWIZZLE_128B (K-major operands),
 // 1 = SWIZZLE_128B_BASE32B (MN-major tf32 operands: the only MN-major layout for tf32)
@@ -78,8 +78,18 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Persistent form: grid = a few CTAs per SM, each looping over work units u = (m tile,
+// n tile, batch entry, split) with stride gridDim.x.  Roles:
+//   warp 0 lane 0 : TMA producer over the (unit, K chunk) sequence (runs ahead across units)
+//   warp 1 lane 0 : MMA issuer; accumulates unit i in TMEM buffer i & 1 (2 x 128 columns)
+//   warps 2..5    : epilogue (warp % 4 = the TMEM lane quarter it may read); drains buffer
+//                   i & 1 while the MMA issuer already fills the other one
+// so TMEM allocation, barrier setup and the epilogue of one unit overlap the next unit's
+// loads and MMAs (the batched updates are tens of thousands of short-K tiles).
+constexpr int TCP_THREADS = 192;
+
 template <int TA, int TB>
-__global__ void __launch_bounds__(TC_THREADS, CD_TC_MINB) k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm) {
+__global__ void __launch_bounds__(TCP_THREADS, CD_TC_MINB) k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm) {
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_tc) + 1023) & ~uintptr_t(1023));
@@ -87,28 +97,40 @@ __global__ void __launch_bounds__(TC_THREADS, CD_TC_MINB) k_gemm_tc32(const Gemm
   unsigned char* Bs = base + TC_STAGES * (TC_BM * TC_BK * 4);  // stages of B (16 KB each)
   uint64_t* full = reinterpret_cast<uint64_t*>(base + TC_STAGES * TC_STAGE_BYTES);
   uint64_t* empty = full + TC_STAGES;
-  uint64_t* accf = empty + TC_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint64_t* accf = empty + TC_STAGES;  // [2] accumulator ready
+  uint64_t* acce = accf + 2;           // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t zb = blockIdx.z;
-  const int split = int(zb % p.splits);
-  const int64_t b = zb / p.splits;
-  const int m0 = blockIdx.x * TC_BM, n0 = blockIdx.y * TC_BN;
-  const int kt0 = split * p.kt_per_split;
-  const int kt1 = min(p.KT, kt0 + p.kt_per_split);
-  const int nkt = kt1 - kt0;
+  const int mt = (p.M + TC_BM - 1) / TC_BM, ntl = (p.N + TC_BN - 1) / TC_BN;
+  const int64_t units = int64_t(mt) * ntl * p.batch * p.splits;
+  auto decode = [&](int64_t u, int& m0, int& n0, int64_t& b, int& split) {
+    const int64_t tmn = int64_t(mt) * ntl;
+    const int64_t zb = u / tmn;
+    const int r = int(u - zb * tmn);
+    m0 = (r % mt) * TC_BM;
+    n0 = (r / mt) * TC_BN;
+    split = int(zb % p.splits);
+    b = zb / p.splits;
+  };
+  auto krange = [&](int split, int& kt0, int& nkt) {
+    kt0 = split * p.kt_per_split;
+    nkt = min(p.KT, kt0 + p.kt_per_split) - kt0;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accf, 1);
+    mbar_init(&accf[0], 1);
+    mbar_init(&accf[1], 1);
+    mbar_init(&acce[0], 4);
+    mbar_init(&acce[1], 4);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 0) {  // TMEM: 128 columns x 128 lanes of fp32 accumulators
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(tmem_slot)));
+  if (warp == 0) {  // TMEM: 2 x 128 columns x 128 lanes of fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -116,120 +138,154 @@ __global__ void __launch_bounds__(TC_THREADS, CD_TC_MINB) k_gemm_tc32(const Gemm
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    for (int it = 0; it < nkt; ++it) {
-      const int s = it % TC_STAGES;
-      if (it >= TC_STAGES) tc_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
-      const int kt = kt0 + it;
-      int sg = 0;
-      if (p.nseg > 1 && kt * TC_BK >= p.seg[1].kv0) sg = 1;
-      if (p.nseg > 2 && kt * TC_BK >= p.seg[2].kv0) sg = 2;
-      const int kl = kt * TC_BK - p.seg[sg].kv0;
-      mbar_expect_tx(&full[s], TC_STAGE_BYTES);
-      unsigned char* as = As + s * (TC_BM * TC_BK * 4);
-      unsigned char* bs = Bs + s * (TC_BN * TC_BK * 4);
-      if (TA == 0) {  // MN-major: four 32(M) x 32(K) boxes
-        for (int c = 0; c < 4; ++c) {
-          if (tm.batched) tma_load_3d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, int(b), &full[s]);
-          else tma_load_2d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, &full[s]);
-        }
-      } else {  // K-major: one 32(K) x 128(M) box
-        if (tm.batched) tma_load_3d(as, &tm.a[sg], kl, m0, int(b), &full[s]);
-        else tma_load_2d(as, &tm.a[sg], kl, m0, &full[s]);
-      }
-      if (TB == 1) {  // MN-major B
-        for (int c = 0; c < 4; ++c) {
-          if (tm.batched) tma_load_3d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, int(b), &full[s]);
-          else tma_load_2d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, &full[s]);
-        }
-      } else {
-        if (tm.batched) tma_load_3d(bs, &tm.b[sg], kl, n0, int(b), &full[s]);
-        else tma_load_2d(bs, &tm.b[sg], kl, n0, &full[s]);
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = tc_idesc(TA == 0 ? 1 : 0, TB == 1 ? 1 : 0);
-    for (int it = 0; it < nkt; ++it) {
-      const int s = it % TC_STAGES;
-      tc_wait(&full[s], (it / TC_STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t sa = smem_u32(As + s * (TC_BM * TC_BK * 4));
-      const uint32_t sb = smem_u32(Bs + s * (TC_BN * TC_BK * 4));
-#pragma unroll
-      for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        // K-major (SW128): advance 32 B along K inside the swizzle atom, 8-row groups 1 KB apart.
-        // MN-major (SW128 with 32 B atoms): K rows 128 B apart, 4-row groups 512 B apart,
-        // 32-element MN chunks 4 KB apart; each K = 8 step starts 8 rows (1 KB) further.
-        const uint64_t da = (TA == 0) ? umma_desc(sa + kk * 1024, 4096, 512, 1) : umma_desc(sa + kk * 32, 16, 1024, 2);
-        const uint64_t db = (TB == 1) ? umma_desc(sb + kk * 1024, 4096, 512, 1) : umma_desc(sb + kk * 32, 16, 1024, 2);
-        const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-        asm volatile(
-            "{\n.reg .pred P;\nsetp.ne.b32 P, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, P;\n}\n" ::"r"(tmem),
-            "l"(da), "l"(db), "r"(idesc), "r"(acc));
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                       smem_u32(&empty[s]))
-                   : "memory");
-    }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                     smem_u32(accf))
-                 : "memory");
-  }
-
-  // ---------------- epilogue: thread = accumulator row ----------------
-  __syncwarp();
-  if (nkt > 0) tc_wait(accf, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const int r = m0 + warp * 32 + lane;
-  float* D = optr_w<float>(p.D, b);
-  const float* Cin = (p.beta != 0.0 && p.splits == 1) ? optr<float>(p.Cin, b) : nullptr;
-  float* part = p.splits > 1
-                    ? reinterpret_cast<float*>(p.part) + (int64_t(split) * p.batch + b) * int64_t(p.M) * p.N
-                    : nullptr;
-  const float alpha = float(p.alpha), beta = float(p.beta);
-#pragma unroll 1
-  for (int cb = 0; cb < TC_BN; cb += 32) {
-    uint32_t v[32];
-    const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(cb);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-          "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    // Cin is usually D itself (in-place update): load the whole chunk first, or every
-    // store would order the next load behind it (one memory latency per column)
-    float cin[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int c = n0 + cb + j;
-      cin[j] = (Cin && r < p.M && c < p.N) ? __ldcg(Cin + r + int64_t(c) * p.Cin.ld) : 0.f;
-    }
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-    if (r < p.M) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int c = n0 + cb + j;
-        const float acc = nkt > 0 ? __uint_as_float(v[j]) : 0.f;
-        if (c < p.N && (!p.tril || r + p.tril - 1 >= c)) {
-          if (part) {
-            part[r + int64_t(c) * p.M] = acc;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int m0, n0, split, kt0, nkt;
+        int64_t b;
+        decode(u, m0, n0, b, split);
+        krange(split, kt0, nkt);
+        for (int kk = 0; kk < nkt; ++kk, ++it) {
+          const int s = it % TC_STAGES;
+          if (it >= TC_STAGES) tc_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
+          const int kt = kt0 + kk;
+          int sg = 0;
+          if (p.nseg > 1 && kt * TC_BK >= p.seg[1].kv0) sg = 1;
+          if (p.nseg > 2 && kt * TC_BK >= p.seg[2].kv0) sg = 2;
+          const int kl = kt * TC_BK - p.seg[sg].kv0;
+          mbar_expect_tx(&full[s], TC_STAGE_BYTES);
+          unsigned char* as = As + s * (TC_BM * TC_BK * 4);
+          unsigned char* bs = Bs + s * (TC_BN * TC_BK * 4);
+          if (TA == 0) {  // MN-major: four 32(M) x 32(K) boxes
+            for (int c = 0; c < 4; ++c) {
+              if (tm.batched) tma_load_3d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, int(b), &full[s]);
+              else tma_load_2d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, &full[s]);
+            }
+          } else {  // K-major: one 32(K) x 128(M) box
+            if (tm.batched) tma_load_3d(as, &tm.a[sg], kl, m0, int(b), &full[s]);
+            else tma_load_2d(as, &tm.a[sg], kl, m0, &full[s]);
+          }
+          if (TB == 1) {  // MN-major B
+            for (int c = 0; c < 4; ++c) {
+              if (tm.batched) tma_load_3d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, int(b), &full[s]);
+              else tma_load_2d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, &full[s]);
+            }
           } else {
-            D[r + int64_t(c) * p.D.ld] = alpha * acc + beta * cin[j];
+            if (tm.batched) tma_load_3d(bs, &tm.b[sg], kl, n0, int(b), &full[s]);
+            else tma_load_2d(bs, &tm.b[sg], kl, n0, &full[s]);
           }
         }
       }
     }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = tc_idesc(TA == 0 ? 1 : 0, TB == 1 ? 1 : 0);
+      int it = 0, i = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        int m0, n0, split, kt0, nkt;
+        int64_t b;
+        decode(u, m0, n0, b, split);
+        krange(split, kt0, nkt);
+        const int buf = i & 1;
+        if (i >= 2) tc_wait(&acce[buf], ((i >> 1) - 1) & 1);  // the epilogue drained this buffer
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t acc_t = tmem + uint32_t(buf * TC_BN);
+        for (int kk = 0; kk < nkt; ++kk, ++it) {
+          const int s = it % TC_STAGES;
+          tc_wait(&full[s], (it / TC_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t sa = smem_u32(As + s * (TC_BM * TC_BK * 4));
+          const uint32_t sb = smem_u32(Bs + s * (TC_BN * TC_BK * 4));
+#pragma unroll
+          for (int k8 = 0; k8 < TC_BK / 8; ++k8) {
+            // K-major (SW128): advance 32 B along K inside the swizzle atom, 8-row groups 1 KB apart.
+            // MN-major (SW128 with 32 B atoms): K rows 128 B apart, 4-row groups 512 B apart,
+            // 32-element MN chunks 4 KB apart; each K = 8 step starts 8 rows (1 KB) further.
+            const uint64_t da = (TA == 0) ? umma_desc(sa + k8 * 1024, 4096, 512, 1) : umma_desc(sa + k8 * 32, 16, 1024, 2);
+            const uint64_t db = (TB == 1) ? umma_desc(sb + k8 * 1024, 4096, 512, 1) : umma_desc(sb + k8 * 32, 16, 1024, 2);
+            const uint32_t acc = (kk > 0 || k8 > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n.reg .pred P;\nsetp.ne.b32 P, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, P;\n}\n" ::"r"(acc_t),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&empty[s]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&accf[buf]))
+                     : "memory");
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5, thread = accumulator row ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const float alpha = float(p.alpha), beta = float(p.beta);
+    int i = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      int m0, n0, split, kt0, nkt;
+      int64_t b;
+      decode(u, m0, n0, b, split);
+      krange(split, kt0, nkt);
+      const int buf = i & 1;
+      tc_wait(&accf[buf], (i >> 1) & 1);  // the MMA issuer commits every unit
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int r = m0 + q * 32 + lane;
+      float* D = optr_w<float>(p.D, b);
+      const float* Cin = (p.beta != 0.0 && p.splits == 1) ? optr<float>(p.Cin, b) : nullptr;
+      float* part = p.splits > 1
+                        ? reinterpret_cast<float*>(p.part) + (int64_t(split) * p.batch + b) * int64_t(p.M) * p.N
+                        : nullptr;
+#pragma unroll 1
+      for (int cb = 0; cb < TC_BN && n0 + cb < p.N; cb += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * TC_BN + cb);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        // Cin is usually D itself (in-place update): load the whole chunk first, or every
+        // store would order the next load behind it (one memory latency per column)
+        float cin[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int c = n0 + cb + j;
+          cin[j] = (Cin && r < p.M && c < p.N) ? __ldcg(Cin + r + int64_t(c) * p.Cin.ld) : 0.f;
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (r < p.M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int c = n0 + cb + j;
+            const float acc = nkt > 0 ? __uint_as_float(v[j]) : 0.f;
+            if (c < p.N && (!p.tril || r + p.tril - 1 >= c)) {
+              if (part) {
+                part[r + int64_t(c) * p.M] = acc;
+              } else {
+                D[r + int64_t(c) * p.D.ld] = alpha * acc + beta * cin[j];
+              }
+            }
+          }
+        }
+      }
+      // buffer drained: let the MMA issuer reuse it
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[buf]);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
 }
 
 }  // namespace cd
