@@ -72,9 +72,10 @@ typedef enum { CD_F64 = 0, CD_F32 = 1 } cd_dtype;
 typedef enum { CD_OP_REV = 0, CD_OP_FWD = 1 } cd_op;
 
 /* Route (the symbolic result may be preferable for small
- * matrices).  AUTO chooses by size; ALGORITHMIC = the paper's unblocked/blocked
- * sweeps; SYMBOLIC = Eq. 10 / Eq. 8 (reverse: small-N
- * batched kernel only, n <= 32). */
+ * matrices).  AUTO = ALGORITHMIC (measured faster on B200 at every size); ALGORITHMIC =
+ * the paper's unblocked/blocked sweeps; SYMBOLIC = Eq. 10
+ * (reverse) / Eq. 8 (forward) on the whole matrix,
+ * one CTA per matrix, offered for n <= 64; larger n return CD_ERR_UNSUPPORTED. */
 typedef enum { CD_ROUTE_AUTO = 0, CD_ROUTE_ALGORITHMIC = 1, CD_ROUTE_SYMBOLIC = 2 } cd_route;
 
 /* Reverse-mode output convention (reading c1):

@@ -34,6 +34,7 @@
 #include "sweep_bulk32.cuh"
 #include "sweep_dmma_cta.cuh"
 #include "symm_ll.cuh"
+#include "symbolic_cta.cuh"
 #include "panel_rev.cuh"
 #include "panel_fwd.cuh"
 #include "gemm_fwd_sk.cuh"
@@ -929,6 +930,17 @@ template <typename T>
 static void drive(Ctx& c, const Call& k) {
   const int n = int(k.n);
   if (n == 0 || k.batch == 0) return;
+  if (k.o.route == CD_ROUTE_SYMBOLIC) {  // n <= SYM_NMAX (checked with the arguments)
+    if (c.plan || !c.ok()) return;
+    const int nblk = (n + 7) / 8;
+    const size_t smem = symbolic_smem(nblk);
+    set_smem(k_symbolic_cta<T>, smem);
+    c.pre(CD_PROF_SWEEP, 0.0);
+    k_symbolic_cta<T><<<unsigned(k.batch), DC_THREADS, smem, c.st>>>(n, k.op == CD_OP_REV ? 1 : 0, k.L, k.A,
+                                                                   k.o.out_mode, k.info);
+    c.launched();
+    return;
+  }
   if (n <= DC_NMAX) {
     run_sweep_small<T>(c, k.op == CD_OP_REV, n, k.batch, k.L, k.A, k.o.out_mode, null_opnd(), k.info);
     return;
@@ -1047,8 +1059,9 @@ static int check_common(cd_op op, int dt, int64_t n, int64_t ldl, int64_t lda, c
 }
 
 static int route_supported(const cd_opts& o, int64_t n) {
-  if (o.route == CD_ROUTE_SYMBOLIC) return CD_ERR_UNSUPPORTED;
-  (void)n;
+  // the symbolic route (Eqs. 8 / 10 on the whole matrix) is offered for small matrices,
+  // where the paper recommends it; larger n use the blocked sweeps
+  if (o.route == CD_ROUTE_SYMBOLIC && n > SYM_NMAX) return CD_ERR_UNSUPPORTED;
   return 0;
 }
 

@@ -90,5 +90,6 @@ def test_workspace_sizes():
 
 
 def test_symbolic_route_unsupported_status():
+    # the symbolic route is offered for n <= 64 only (include/choldiff.h); larger n: CD_ERR_UNSUPPORTED
     o = cd._Opts(0, 2, 0, 0)
-    assert _rev(4, 4, 4, opts=ctypes.byref(o)) == 2
+    assert _rev(65, 65, 65, opts=ctypes.byref(o)) == 2

@@ -180,3 +180,34 @@ def test_host_buffer_path():
     Ah = torch.from_numpy(synthetic.to_colmajor(Lb)).transpose(0, 1).pin_memory()
     cd.chol_host("rev", Lh, Ah)
     assert nerr(Ah.numpy(), oracle.chol_rev(L, Lb)) < TOL64
+
+
+@pytest.mark.parametrize("n", [1, 5, 8, 17, 32, 33, 64])
+def test_symbolic_route(n):
+    # north star (d) / PAPER.md:748-754: Eq. 10 (reverse) and Eq. 8 (forward) on the whole matrix
+    B = 5
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=70 + n, sdot=True)
+    r = cd.chol_rev(to_dev(L), to_dev(Lb), route="symbolic")
+    assert nerr(to_host(r), oracle_rev(L, Lb)) < TOL64
+    f = cd.chol_fwd(to_dev(L), to_dev(np.tril(Sd)), route="symbolic")
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
+    for mode in ("sym", "grad"):  # output conventions through the same store
+        a = to_host(cd.chol_rev(to_dev(L), to_dev(Lb), route="symbolic", out=mode))
+        b = to_host(cd.chol_rev(to_dev(L), to_dev(Lb), out=mode))
+        assert np.abs(a - b).max() / np.linalg.norm(b.reshape(B, -1), axis=1).min() < TOL64
+    # fp32 on the rounded inputs
+    L32, Lb32 = fp32_round(L, Lb)
+    r32 = cd.chol_rev(to_dev(L32, torch.float32), to_dev(Lb32, torch.float32), route="symbolic")
+    assert nerr(to_host(r32), oracle_rev(L32, Lb32)) < TOL32
+
+
+def test_symbolic_route_upper_never_read_and_limits():
+    n = 40
+    L, Lb, _ = synthetic.draw(n, 4)
+    out = to_host(cd.chol_rev(to_dev(synthetic.poison_upper(L)), to_dev(synthetic.poison_upper(Lb)),
+                              route="symbolic"))
+    assert np.all(np.isnan(out[np.triu_indices(n, 1)]))
+    assert nerr(out, oracle.chol_rev(L, Lb)) < TOL64
+    L, Lb, _ = synthetic.draw(65, 4)
+    with pytest.raises(cd.CholdiffError):
+        cd.chol_rev(to_dev(L), to_dev(Lb), route="symbolic")
