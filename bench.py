@@ -433,6 +433,12 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
                         "algorithmic_bytes_per_matrix": algo_bytes,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs", "traffic": load_traffic("bulk32")},
            "gpu_launches": int(launches), "clocks": clk.summary()}
+    # the symbolic route (Eq. 10 on the whole matrix, north star (d)) on the same inputs, for
+    # the route choice "by measurement" (AUTO = algorithmic)
+    sms = timed_steps(lambda: cd.chol_rev(Ld, A, route="symbolic"), restore, 5, 2, dist, stream)
+    out["symbolic_route"] = {"ms_per_step": round(dist.max(statistics.mean(sms)), 4),
+                             "matrices_per_s": round(total / (dist.max(statistics.mean(sms)) * 1e-3), 1),
+                             "kernel": "k_symbolic_cta (one CTA per matrix, Eq. 10 on 8x8 DMMA tiles)"}
     if gather and P > 1:
         # NCCL used only to gather the sharded results (north star), timed separately
         torch.cuda.synchronize()
