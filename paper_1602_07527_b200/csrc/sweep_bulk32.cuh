@@ -18,9 +18,9 @@
 //     registers, Abar has two buffers: the next matrix streams in during the compute;
 //   * the remaining layout changes (transposes) go through an 8x8 shared-memory scratch
 //     tile of pitch 10 (one 16-byte store + two loads, conflict free) instead of shuffles;
-//   * results go back through shared memory as coalesced 16-byte stores of the lower
-//     triangle only (the one row above the diagonal that an odd column's copy fetched is
-//     never used and never written).
+//   * results are stored straight from the accumulator layout (each warp store covers 4
+//     columns x 64 contiguous bytes), lower triangle only; the one row above the diagonal
+//     that an odd column's copy fetched is never used and never written.
 #pragma once
 #include "common.cuh"
 #include "sweep_reg32.cuh"
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(B32_WPB * 32, 3)
   for (int it = 0; b < batch; b += stride, ++it) {
     const int k = it & 1;
     const bool more = b + stride < batch;
-    if (more) copy_in(sAb(k ^ 1), Ad, b + stride);  // buffer k^1's previous stores were synchronous
+    if (more) copy_in(sAb(k ^ 1), Ad, b + stride);  // buffer k^1's last use ended with the previous matrix
     if (more) cp_async_wait<1>();                     // all but the group just issued
     else cp_async_wait<0>();
     __syncwarp();
@@ -251,38 +251,32 @@ __global__ void __launch_bounds__(B32_WPB * 32, 3)
         if (g >= 2 * t) Dbar[0] -= p0 + q0;
         if (g >= 2 * t + 1) Dbar[1] -= p1 + q1;
       }
-      // s4: Dbar <- Phi(D^{-T}(P + P^T)D^{-1}), P = Phi(D^T Dbar); S = D^{-T}(P+P^T)D^{-1}  (Eq. 10)
+      // s4: Dbar <- Phi(D^{-T} X D^{-1}), X = P + P^T, P = Phi(M), M = D^T Dbar;  S = D^{-T} X D^{-1}
+      //     (Eq. 10).  One transpose (Dbar's B layout) serves both M = D^T Dbar and
+      //     M^T = Dbar^T D, so X = P + P^T is formed in the C layout without another; X is
+      //     symmetric, so its B layout equals its C layout and W = D^{-T} X, Y = W D^{-1}
+      //     need no layout change either.
       double s0, s1;
       {
         double* T0 = S + (NBLK - 1) * SC_TILE;  // s1 uses at most tiles 0 .. NBLK-2
         sc_put(T0, g, t, Dbar[0], Dbar[1]);
         __syncwarp();
         double b0, b1;
-        sc_getT(T0, g, t, b0, b1);
+        sc_getT(T0, g, t, b0, b1);  // Dbar(2t + kk, g)
         const double* D = Lt[TI(J, J)];
-        double p0 = 0.0, p1 = 0.0;
-        dmma884(p0, p1, D[0], b0);  // D^T Dbar: A(g, k) = D(k, g) = B layout of D
-        dmma884(p0, p1, D[1], b1);
+        double m0 = 0.0, m1 = 0.0, n0 = 0.0, n1 = 0.0;
+        dmma884(m0, m1, D[0], b0);  // M = D^T Dbar
+        dmma884(m0, m1, D[1], b1);
+        dmma884(n0, n1, b0, D[0]);  // M^T = Dbar^T D
+        dmma884(n0, n1, b1, D[1]);
         const int c0 = 2 * t, c1 = 2 * t + 1;
-        p0 = (g > c0) ? p0 : (g == c0 ? 0.5 * p0 : 0.0);
-        p1 = (g > c1) ? p1 : (g == c1 ? 0.5 * p1 : 0.0);
-        __syncwarp();
-        sc_put(T0, g, t, p0, p1);
-        __syncwarp();
-        double pt0, pt1;  // X = P + P^T in A (= C) layout
-        sc_getT(T0, g, t, pt0, pt1);
-        const double xa0 = p0 + pt0, xa1 = p1 + pt1;
-        double z0 = 0.0, z1 = 0.0;  // Z = X D^{-1}
-        dmma884(z0, z1, xa0, di0);
-        dmma884(z0, z1, xa1, di1);
-        __syncwarp();
-        sc_put(T0, g, t, z0, z1);
-        __syncwarp();
-        double zb0, zb1;
-        sc_getT(T0, g, t, zb0, zb1);
-        double y0 = 0.0, y1 = 0.0;  // Y = D^{-T} Z: A(g, k) = Dinv(k, g)
-        dmma884(y0, y1, di0, zb0);
-        dmma884(y0, y1, di1, zb1);
+        const double x0 = g >= c0 ? m0 : n0, x1 = g >= c1 ? m1 : n1;  // X = Phi(M) + Phi(M)^T
+        double w0 = 0.0, w1 = 0.0;  // W = D^{-T} X
+        dmma884(w0, w1, di0, x0);
+        dmma884(w0, w1, di1, x1);
+        double y0 = 0.0, y1 = 0.0;  // Y = W D^{-1}
+        dmma884(y0, y1, w0, di0);
+        dmma884(y0, y1, w1, di1);
         s0 = y0;  // S = Y in A (= C) layout, for s5
         s1 = y1;
         Dbar[0] = (g > c0) ? y0 : (g == c0 ? 0.5 * y0 : 0.0);
@@ -310,30 +304,19 @@ __global__ void __launch_bounds__(B32_WPB * 32, 3)
       __syncwarp();  // scratch reads of this step done before the next step's stores
     }
 
-    // ---- stage tril(Sigma_bar) in the Abar buffer, then coalesced 16-byte stores
+    // ---- tril(Sigma_bar) straight from the C-layout registers: per tile two warp stores,
+    //      each 4 columns x 64 contiguous bytes; the upper triangle is never written
+    {
+      double* Ag = optr_w<double>(Ad, b);
 #pragma unroll
-    for (int bj = 0; bj < NBLK; ++bj)
+      for (int bj = 0; bj < NBLK; ++bj)
 #pragma unroll
-      for (int bi = bj; bi < NBLK; ++bi)
+        for (int bi = bj; bi < NBLK; ++bi)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
-          if (bi > bj || r >= c) sA[bC[bj][e] + r] = Ac[TI(bi, bj)][e];
-        }
-    __syncwarp();
-    double* Ag = optr_w<double>(Ad, b);
-#pragma unroll
-    for (int c0 = 0; c0 < N; c0 += 2) {  // half-warp per column, lane & 15 = row pair
-      const int c = c0 + (lane >> 4), r = 2 * (lane & 15);
-      if (r < N && r >= (c & ~1)) {
-        const double2 v = *reinterpret_cast<const double2*>(sA + base[c] + r);
-        double* dst = Ag + r + int64_t(c) * Ad.ld;
-        if (r >= c) {
-          *reinterpret_cast<double2*>(dst) = v;
-        } else {  // odd column, first pair: row c - 1 is above the diagonal
-          dst[1] = v.y;
-        }
-      }
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * bi + g, c = 8 * bj + 2 * t + e;
+            if (bi > bj || r >= c) Ag[r + int64_t(c) * Ad.ld] = Ac[TI(bi, bj)][e];
+          }
     }
     __syncwarp();
   }
