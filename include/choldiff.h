@@ -143,6 +143,12 @@ size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const 
 size_t cd_workspace_size_host(cd_op op, cd_dtype dt, int64_t n, const cd_opts* opts);
 int cd_chol_host(cd_op op, cd_dtype dt, int64_t n, const void* L_host, void* A_host,
                  const cd_opts* opts, void* ws, size_t ws_bytes, cd_stream_t stream);
+/* Bytes the last cd_chol_host call on this thread moved host -> device and device -> host.
+ * fp64 with the fused nb = 128 schedules and TRIL output (the default) pipelines the copies:
+ * the lower part of each 128-column block streams in on a library copy stream just before
+ * the sweep needs it and streams out as soon as it is final, so only the lower triangles
+ * (plus the diagonal blocks once more) cross the bus; other cases copy the dense arrays. */
+void cd_host_bytes(int64_t* h2d, int64_t* d2h);
 
 /* Diagnostic entry point (kernel validation): C = alpha * op(A) op(B) + beta * C with the
  * library's Level-3 kernel family (op = transpose when ta / tb = 1), column-major, device

@@ -27,7 +27,7 @@ import torch
 from . import _build
 
 __all__ = ["chol_rev", "chol_fwd", "chol_host", "colmajor", "workspace_size", "lib", "library_path",
-           "launch_count", "reset_launch_count", "CholdiffError", "OUT_MODES", "ROUTES"]
+           "launch_count", "reset_launch_count", "CholdiffError", "OUT_MODES", "ROUTES", "host_bytes"]
 
 CD_F64, CD_F32 = 0, 1
 CD_OP_REV, CD_OP_FWD = 0, 1
@@ -238,3 +238,10 @@ def chol_host(op: str, L_host: torch.Tensor, A_host: torch.Tensor, *, nb=None, d
         _check(rc)
         stream.synchronize()
     return A_host
+
+
+def host_bytes():
+    """(h2d, d2h) bytes moved by the last chol_host call on this thread (cd_host_bytes)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    lib().cd_host_bytes(ctypes.byref(a), ctypes.byref(b))
+    return int(a.value), int(b.value)

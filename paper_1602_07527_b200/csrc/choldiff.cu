@@ -104,6 +104,89 @@ static int note_cuda(cudaError_t e) {
   return CD_ERR_CUDA;
 }
 
+// ---- host-buffer pipeline (cd_chol_host): column blocks stream in / out while the sweep runs ----
+// Only the lower part of each column block, rows [j, n) of columns [j, j+w), is moved:
+// the contract never reads the upper triangles, and TRIL output never writes them.
+struct HostPipe {
+  cudaStream_t cin = nullptr, cout = nullptr;  // library copy streams (per device)
+  const char* Lh = nullptr;                    // host L (column-major, ld n)
+  const char* Ah_in = nullptr;                 // host input triangle
+  char* Ah = nullptr;                          // host output
+  char* dL = nullptr;                          // device copies (ld n)
+  char* dA = nullptr;
+  int64_t n = 0;
+  size_t es = 8;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  cudaEvent_t ev() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+  size_t off(int64_t r, int64_t c) const { return (size_t(r) + size_t(c) * size_t(n)) * es; }
+  // diagonal blocks of L first (the block inverses need all of them), then column blocks in
+  // the order `order` lists them; returns one event per column block
+  void h2d(int nblk, int nb, bool reverse, std::vector<cudaEvent_t>& ev_in, cudaEvent_t& ev_diag);
+  // after `compute` has finished column block [j, j+w): copy rows [j, n) back
+  void d2h(cudaStream_t compute, int j, int w) {
+    cudaEvent_t e = ev();
+    cudaEventRecord(e, compute);
+    cudaStreamWaitEvent(cout, e, 0);
+    cudaMemcpy2DAsync(Ah + off(j, j), size_t(n) * es, dA + off(j, j), size_t(n) * es, size_t(n - j) * es, size_t(w),
+                      cudaMemcpyDeviceToHost, cout);
+  }
+  int64_t bytes_in = 0, bytes_out = 0;
+};
+static thread_local HostPipe* g_pipe = nullptr;
+
+struct HostStreams {
+  cudaStream_t cin = nullptr, cout = nullptr;
+  HostPipe pipe;
+};
+static thread_local HostStreams g_hs[64];
+static bool g_no_host_pipe = getenv("CD_NO_HOST_PIPE") != nullptr;
+static thread_local int64_t g_host_bytes_in = 0, g_host_bytes_out = 0;
+
+static HostStreams* host_streams() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  HostStreams& s = g_hs[dev];
+  if (!s.cin) {
+    if (cudaStreamCreateWithFlags(&s.cin, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaStreamCreateWithFlags(&s.cout, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  }
+  return &s;
+}
+
+
+void HostPipe::h2d(int nblk, int nb, bool reverse, std::vector<cudaEvent_t>& ev_in, cudaEvent_t& ev_diag) {
+  for (int qb = 0; qb < nblk; ++qb) {
+    int j, w;
+    block_range(int(n), nb, reverse, qb, j, w);
+    cudaMemcpy2DAsync(dL + off(j, j), size_t(n) * es, Lh + off(j, j), size_t(n) * es, size_t(w) * es, size_t(w),
+                      cudaMemcpyHostToDevice, cin);
+    bytes_in += int64_t(w) * w * int64_t(es);
+  }
+  ev_diag = ev();
+  cudaEventRecord(ev_diag, cin);
+  ev_in.assign(size_t(nblk), nullptr);
+  for (int i = 0; i < nblk; ++i) {
+    const int qb = reverse ? nblk - 1 - i : i;
+    int j, w;
+    block_range(int(n), nb, reverse, qb, j, w);
+    cudaMemcpy2DAsync(dL + off(j, j), size_t(n) * es, Lh + off(j, j), size_t(n) * es, size_t(n - j) * es, size_t(w),
+                      cudaMemcpyHostToDevice, cin);
+    cudaMemcpy2DAsync(dA + off(j, j), size_t(n) * es, Ah_in + off(j, j), size_t(n) * es, size_t(n - j) * es,
+                      size_t(w), cudaMemcpyHostToDevice, cin);
+    bytes_in += 2 * int64_t(n - j) * w * int64_t(es);
+    ev_in[size_t(qb)] = ev();
+    cudaEventRecord(ev_in[size_t(qb)], cin);
+  }
+}
+
 struct Ctx {
   bool plan;            // plan mode: carve workspace only
   char* ws;             // device workspace base (run mode)
@@ -699,6 +782,12 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       return;
     }
   }
+  std::vector<cudaEvent_t> ev_in;
+  if (g_pipe) {  // host path: diagonal blocks, then column blocks right to left, stream in
+    cudaEvent_t ev_diag;
+    g_pipe->h2d(nblk, nb, true, ev_in, ev_diag);
+    cudaStreamWaitEvent(c.st, ev_diag, 0);
+  }
   c.err = note_cuda(cudaMemsetAsync(cnt, 0, sizeof(int) * size_t(batch) * nblk, c.st));
   set_smem(k_symm_ll, LL_SMEM);
   run_trinv<double>(c, n, nb, true, batch, L, Dinv);
@@ -706,6 +795,7 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     int j, w;
     block_range(n, nb, true, qb, j, w);
     const int k = j + w, p = n - k;
+    if (g_pipe) cudaStreamWaitEvent(c.st, ev_in[size_t(qb)], 0);
     if (p > 0) {
       LLParams lp;
       lp.A = A;
@@ -749,6 +839,7 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     c.err = note_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_panel_rev), dim3(grid),
                                                   dim3(PR_THREADS), args, PR_SMEM, c.st));
     c.launched();
+    if (g_pipe) g_pipe->d2h(c.st, j, w);  // column block final: stream it out
   }
   if (info && c.ok()) {
     c.pre(CD_PROF_OTHER, 0.0);
@@ -849,6 +940,12 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       return;
     }
   }
+  std::vector<cudaEvent_t> ev_in;
+  if (g_pipe) {  // host path: diagonal blocks, then column blocks left to right, stream in
+    cudaEvent_t ev_diag;
+    g_pipe->h2d(nblk, nb, false, ev_in, ev_diag);
+    cudaStreamWaitEvent(c.st, ev_diag, 0);
+  }
   c.err = note_cuda(cudaMemsetAsync(cnt, 0, sizeof(int) * size_t(batch) * nblk, c.st));
   set_smem(k_fwd_sk, FS_SMEM);
   set_smem(k_panel_fwd, PR_SMEM);
@@ -858,6 +955,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     int j, w;
     block_range(n, nb, false, qb, j, w);
     const int k = j + w, p = n - k, q = j;
+    if (g_pipe) cudaStreamWaitEvent(c.st, ev_in[size_t(qb)], 0);
     PanelFwdParams pf;
     pf.A = A;
     pf.L = L;
@@ -881,6 +979,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     c.err = note_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_panel_fwd), dim3(grid),
                                                   dim3(PR_THREADS), args, PR_SMEM, c.st));
     c.launched();
+    if (g_pipe && qb > 0) g_pipe->d2h(c.st, j_prev, 128);  // previous block's W D^{-T} is done
     if (p > 0 && c.ok()) {
       FSParams fp;
       fp.A = A;
@@ -900,6 +999,11 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       c.launched();
     }
     j_prev = j, k_prev = k, p_prev = p;
+  }
+  if (g_pipe && c.ok()) {  // the last block (no rows below it) is final after its panel
+    int j, w;
+    block_range(n, nb, false, nblk - 1, j, w);
+    g_pipe->d2h(c.st, j, w);
   }
   if (info && c.ok()) {
     c.pre(CD_PROF_OTHER, 0.0);
@@ -1169,6 +1273,47 @@ int cd_chol_host(cd_op op, cd_dtype dt, int64_t n, const void* L_host, void* A_h
   char* dL = static_cast<char*>(ws);
   char* dA = dL + mat;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const cd_opts o = opts ? *opts : kDefaultOpts;
+  // pipelined path: the fused fp64 schedules (nb = 128, TRIL output, even n for TMA) stream
+  // column blocks in and out while they run
+  if (dt == CD_F64 && (o.nb == 0 || o.nb == 128) && o.out_mode == CD_OUT_TRIL && o.route != CD_ROUTE_SYMBOLIC &&
+      n > DC_NMAX && n % 2 == 0 && !g_no_ll && !g_tma_disabled && !g_no_host_pipe) {
+    HostStreams* hs = host_streams();
+    if (hs) {
+      HostPipe& hp = hs->pipe;
+      hp.cin = hs->cin;
+      hp.cout = hs->cout;
+      hp.Lh = static_cast<const char*>(L_host);
+      hp.Ah_in = static_cast<const char*>(A_host);
+      hp.Ah = static_cast<char*>(A_host);
+      hp.dL = dL;
+      hp.dA = dA;
+      hp.n = n;
+      hp.es = es;
+      hp.next = 0;
+      hp.bytes_in = hp.bytes_out = 0;
+      // the copy streams must not start before work already queued on `stream`
+      cudaEvent_t e0 = hp.ev();
+      cudaEventRecord(e0, st);
+      cudaStreamWaitEvent(hp.cin, e0, 0);
+      cudaStreamWaitEvent(hp.cout, e0, 0);
+      g_pipe = &hp;
+      void* ws2 = dA + mat;
+      const size_t ws2b = ws_bytes - 2 * mat;
+      const int r = (op == CD_OP_REV) ? cd_chol_rev(dt, n, dL, n, dA, n, opts, ws2, ws2b, nullptr, stream)
+                                      : cd_chol_fwd(dt, n, dL, n, dA, n, opts, ws2, ws2b, nullptr, stream);
+      g_pipe = nullptr;
+      cudaEvent_t e1 = hp.ev();  // `stream` completes only after the last copy out
+      cudaEventRecord(e1, hp.cout);
+      cudaStreamWaitEvent(st, e1, 0);
+      g_host_bytes_in = hp.bytes_in;
+      g_host_bytes_out = 0;
+      for (int64_t j = 0; j < n; j += 128) g_host_bytes_out += (n - j) * std::min<int64_t>(128, n - j) * int64_t(es);
+      return r;
+    }
+  }
+  g_host_bytes_in = 2 * n * n * int64_t(es);
+  g_host_bytes_out = n * n * int64_t(es);
   int r = note_cuda(cudaMemcpyAsync(dL, L_host, size_t(n) * n * es, cudaMemcpyHostToDevice, st));
   if (r) return r;
   r = note_cuda(cudaMemcpyAsync(dA, A_host, size_t(n) * n * es, cudaMemcpyHostToDevice, st));
@@ -1212,6 +1357,10 @@ const char* cd_status_string(int status) {
 }
 
 const char* cd_last_cuda_error(void) { return g_cuda_err; }
+void cd_host_bytes(int64_t* h2d, int64_t* d2h) {
+  if (h2d) *h2d = g_host_bytes_in;
+  if (d2h) *d2h = g_host_bytes_out;
+}
 int cd_version(void) { return CD_VERSION; }
 int64_t cd_launch_count(void) { return g_launches; }
 

@@ -173,13 +173,30 @@ def test_deterministic():
     assert np.array_equal(np.tril(a), np.tril(b))
 
 
-def test_host_buffer_path():
-    n = 300
-    L, Lb, _ = synthetic.draw(n, 8)
-    Lh = torch.from_numpy(synthetic.to_colmajor(L)).transpose(0, 1).pin_memory()
-    Ah = torch.from_numpy(synthetic.to_colmajor(Lb)).transpose(0, 1).pin_memory()
+@pytest.mark.parametrize("n", [200, 300, 301, 1024])
+def test_host_buffer_path(n):
+    # even n: the pipelined copies (lower part of each column block streamed in / out);
+    # odd n: dense copies.  Upper triangles are NaN-poisoned and must come back untouched.
+    L, Lb, Sd = synthetic.draw(n, 8 + n, sdot=True)
+
+    def host(m):
+        return torch.from_numpy(synthetic.to_colmajor(synthetic.poison_upper(m))).transpose(0, 1).pin_memory()
+
+    iu = np.triu_indices(n, 1)
+    Lh, Ah = host(L), host(Lb)
     cd.chol_host("rev", Lh, Ah)
-    assert nerr(Ah.numpy(), oracle.chol_rev(L, Lb)) < TOL64
+    out = Ah.numpy()
+    assert nerr(out, oracle.chol_rev(L, Lb)) < TOL64
+    assert np.all(np.isnan(out[iu]))
+    h2d, d2h = cd.host_bytes()
+    assert 0 < d2h <= n * n * 8 and h2d > 0
+    if n >= 1024:  # pipelined: lower triangles (+ the diagonal blocks once more) only
+        assert h2d < 0.7 * 2 * n * n * 8 and d2h < 0.7 * n * n * 8
+    Fh = host(np.tril(Sd))
+    cd.chol_host("fwd", host(L), Fh)
+    f = Fh.numpy()
+    assert nerr(f, oracle_fwd(L, Sd)) < TOL64
+    assert np.all(np.isnan(f[iu]))
 
 
 @pytest.mark.parametrize("n", [1, 5, 8, 17, 32, 33, 64])
