@@ -750,6 +750,7 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
   double* prpart = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
   double* Pws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   double* Zws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
+  double* Wst = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
   (void)part_ws;
   if (c.plan || !c.ok()) return;
   set_smem(k_panel_rev, PR_SMEM);
@@ -832,6 +833,7 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pp.s_ld = LL_BM + 4;
     pp.s_stride = s_stride;
     pp.dbg_skip = g_dbg_panel_skip;
+    pp.Wst = Wst;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs
     void* args[] = {&pp};
     const double wf = w;

@@ -55,6 +55,7 @@ struct PanelParams {
   int s_ld;
   int64_t s_stride;
   int dbg_skip;  // measurement only (CD_DEBUG_PANEL_SKIP): bit i skips phase i+1; results wrong
+  double* Wst;   // small-panel phase 1 staging of W: [batch * tiles][128 * 128]
 };
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
@@ -114,8 +115,67 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   const int wm = warp >> 2, wn = wm == 0 ? (warp & 3) : 3 - (warp & 3), g = lane >> 2, t = lane & 3;
   const int w = p.w;
   const int64_t units = p.batch * p.tiles;
+  // few tiles (early steps): split every tile's work into 32 x 32 tiles over the grid --
+  // 1a: W = Cbar D^{-1} (16 tiles per 128-row tile, staged), grid sync, 1b: the lower
+  // 32 x 32 tiles of P_t = W^T C (K = the tile's 128 rows) and W copied back in place
+  const bool small = units * 4 <= int64_t(gridDim.x);
+  if (small && !(p.dbg_skip & 1)) {
+    const int64_t ua = units * 16;
+    for (int64_t u = blockIdx.x; u < ua; u += gridDim.x) {
+      const int64_t bt = u >> 4;
+      const int64_t b = bt / p.tiles;
+      const int tl = int(bt - b * p.tiles);
+      const int ti = int(u & 15) >> 2, tj = int(u & 3);
+      const int r0 = p.k + 128 * tl + 32 * ti, c0 = 32 * tj;
+      const double* Cb = optr<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;
+      const double* Di = p.Dinv + b * p.dstride;
+      double* st = p.Wst + bt * (128 * 128) + 32 * ti;  // staging, ld 128
+      pr_tile32(
+          sm, [&](int m, int k) -> const double* { return k < w ? Cb + m + int64_t(k) * p.A.ld : nullptr; },
+          [&](int k, int n) -> const double* {  // D^{-1}(k, c0 + n), zero above the diagonal
+            const int cc = c0 + n;
+            return (k < w && cc < w && k >= cc) ? Di + k + int64_t(cc) * p.dld : nullptr;
+          },
+          [&](int m, int n, double v) { __stcg(st + m + (c0 + n) * 128, v); });
+    }
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+    const int64_t ub = units * 11;  // 10 lower P_t tiles + 1 copy-back unit per 128-row tile
+    for (int64_t u = blockIdx.x; u < ub; u += gridDim.x) {
+      const int64_t bt = u / 11;
+      const int lt = int(u - bt * 11);
+      const int64_t b = bt / p.tiles;
+      const int tl = int(bt - b * p.tiles);
+      const int r0 = p.k + 128 * tl;
+      const double* Wb = p.Wst + bt * (128 * 128);
+      if (lt == 10) {  // W -> Abar (in place of Cbar)
+        double* Cb = optr_w<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;
+        for (int e = tid; e < 128 * w; e += PR_THREADS) {
+          const int r = e & 127, c = e >> 7;
+          Cb[r + int64_t(c) * p.A.ld] = __ldcg(Wb + e);
+        }
+        continue;
+      }
+      int ti = 0, tj = 0;  // lower tile lt -> (ti >= tj)
+      {
+        int r = lt;
+        while (r > ti) r -= ++ti;
+        tj = r;
+      }
+      const double* Ct = optr<double>(p.L, b) + r0 + int64_t(p.j) * p.L.ld;
+      double* slot = p.part + bt * int64_t(128 * 128);
+      const int a0 = 32 * ti, c0 = 32 * tj;
+      pr_tile32(
+          sm, [&](int m, int k) -> const double* { return (a0 + m < w) ? Wb + k + (a0 + m) * 128 : nullptr; },
+          [&](int k, int n) -> const double* { return (c0 + n < w) ? Ct + k + int64_t(c0 + n) * p.L.ld : nullptr; },
+          [&](int m, int n, double v) {
+            const int a = a0 + m, cc = c0 + n;
+            if (a >= cc) __stcg(slot + a + cc * 128, v);
+          });
+    }
+  }
 
-  for (int64_t u = blockIdx.x; u < units && !(p.dbg_skip & 1); u += gridDim.x) {
+  for (int64_t u = blockIdx.x; u < units && !small && !(p.dbg_skip & 1); u += gridDim.x) {
     const int64_t b = u / p.tiles;
     const int tl = int(u - b * p.tiles);
     const int r0 = p.k + 128 * tl;
