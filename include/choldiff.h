@@ -69,7 +69,7 @@ extern "C" {
 typedef struct CUstream_st* cd_stream_t; /* == cudaStream_t */
 
 typedef enum { CD_F64 = 0, CD_F32 = 1 } cd_dtype;
-typedef enum { CD_OP_REV = 0, CD_OP_FWD = 1 } cd_op;
+typedef enum { CD_OP_REV = 0, CD_OP_FWD = 1, CD_OP_CHOL_FWD = 2 } cd_op;
 
 /* Route (the symbolic result may be preferable for small
  * matrices).  AUTO = ALGORITHMIC (measured faster on B200 at every size); ALGORITHMIC =
@@ -143,6 +143,24 @@ size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const 
 size_t cd_workspace_size_host(cd_op op, cd_dtype dt, int64_t n, const cd_opts* opts);
 int cd_chol_host(cd_op op, cd_dtype dt, int64_t n, const void* L_host, void* A_host,
                  const cd_opts* opts, void* ws, size_t ws_bytes, cd_stream_t stream);
+/* Fused factorisation + forward mode: chol_blocked and
+ * chol_blocked_fwd accumulated in one sweep, as PAPER.md:501-503 and
+ * 649-651 suggest ("these updates could be accumulated at the same time as computing the
+ * original Cholesky decomposition").
+ *   in:  tril(A) = tril(Sigma) (Sigma symmetric positive definite), tril(Adot) = tril(Sigma_dot)
+ *   out: tril(A) = L with Sigma = L L^T, tril(Adot) = Ldot
+ * Both in place, column-major, only lower triangles read or written.  fp64 only (fp32 returns
+ * CD_ERR_UNSUPPORTED); n <= 128 runs on chip, larger n needs the fused nb = 128 schedule:
+ * 16-byte aligned arrays with even ld (otherwise CD_ERR_UNSUPPORTED).  d_info[b] = j > 0 if
+ * the j-th (1-based) pivot of the factorisation was not positive (Sigma not positive
+ * definite); outputs are then unspecified.  Workspace: cd_workspace_size(CD_OP_CHOL_FWD, ...). */
+int cd_chol_fwd_fused(cd_dtype dt, int64_t n, void* A, int64_t lda, void* Adot, int64_t ldadot,
+                      const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream);
+int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t lda, int64_t strideA,
+                                      void* Adot, int64_t ldadot, int64_t strideAdot, int64_t batch,
+                                      const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
+                                      cd_stream_t stream);
+
 /* Bytes the last cd_chol_host call on this thread moved host -> device and device -> host.
  * fp64 with the fused nb = 128 schedules and TRIL output (the default) pipelines the copies:
  * the lower part of each 128-column block streams in on a library copy stream just before

@@ -27,10 +27,11 @@ import torch
 from . import _build
 
 __all__ = ["chol_rev", "chol_fwd", "chol_host", "colmajor", "workspace_size", "lib", "library_path",
-           "launch_count", "reset_launch_count", "CholdiffError", "OUT_MODES", "ROUTES", "host_bytes"]
+           "launch_count", "reset_launch_count", "CholdiffError", "OUT_MODES", "ROUTES", "host_bytes",
+           "chol_fwd_fused"]
 
 CD_F64, CD_F32 = 0, 1
-CD_OP_REV, CD_OP_FWD = 0, 1
+CD_OP_REV, CD_OP_FWD, CD_OP_CHOL_FWD = 0, 1, 2
 ROUTES = {"auto": 0, "algorithmic": 1, "symbolic": 2}
 OUT_MODES = {"tril": 0, "sym": 1, "grad": 2}
 
@@ -70,6 +71,11 @@ def lib():
                 f = getattr(L, name)
                 f.argtypes = [ctypes.c_int, i64, vp, i64, i64, vp, i64, i64, i64, po, vp, sz, vp, vp]
                 f.restype = ctypes.c_int
+            L.cd_chol_fwd_fused.argtypes = [ctypes.c_int, i64, vp, i64, vp, i64, po, vp, sz, vp, vp]
+            L.cd_chol_fwd_fused.restype = ctypes.c_int
+            L.cd_chol_fwd_fused_strided_batched.argtypes = [ctypes.c_int, i64, vp, i64, i64, vp, i64, i64, i64, po,
+                                                             vp, sz, vp, vp]
+            L.cd_chol_fwd_fused_strided_batched.restype = ctypes.c_int
             for name in ("cd_chol_rev_batched", "cd_chol_fwd_batched"):
                 f = getattr(L, name)
                 f.argtypes = [ctypes.c_int, i64, vp, i64, vp, i64, i64, po, vp, sz, vp, vp]
@@ -188,11 +194,14 @@ def _run(op: int, L: torch.Tensor, A: torch.Tensor, nb, route, out, info: bool):
         lda = max(1, A.stride(-1)) if n > 1 else max(1, n)
         wsp = ctypes.c_void_p(ws.data_ptr()) if ws is not None else None
         ip = ctypes.c_void_p(info_t.data_ptr()) if info_t is not None else None
+        single = {CD_OP_REV: Lc.cd_chol_rev, CD_OP_FWD: Lc.cd_chol_fwd, CD_OP_CHOL_FWD: Lc.cd_chol_fwd_fused}
+        strided = {CD_OP_REV: Lc.cd_chol_rev_strided_batched, CD_OP_FWD: Lc.cd_chol_fwd_strided_batched,
+                   CD_OP_CHOL_FWD: Lc.cd_chol_fwd_fused_strided_batched}
         if A.dim() == 2:
-            f = Lc.cd_chol_rev if op == CD_OP_REV else Lc.cd_chol_fwd
+            f = single[op]
             rc = f(dt, n, L.data_ptr(), ldl, A.data_ptr(), lda, ctypes.byref(o), wsp, nbytes, ip, stream)
         else:
-            f = Lc.cd_chol_rev_strided_batched if op == CD_OP_REV else Lc.cd_chol_fwd_strided_batched
+            f = strided[op]
             sL = L.stride(0) if batch > 1 else ldl * n
             sA = A.stride(0) if batch > 1 else lda * n
             rc = f(dt, n, L.data_ptr(), ldl, sL, A.data_ptr(), lda, sA, batch, ctypes.byref(o), wsp, nbytes, ip,
@@ -215,6 +224,20 @@ def chol_fwd(L: torch.Tensor, Sdot: torch.Tensor, *, nb=None, route: str = "auto
     """Forward mode (L, Sigma_dot) -> L_dot (lower triangle of the returned tensor)."""
     L, A = _prep(L, Sdot, inplace)
     return _run(CD_OP_FWD, L, A, nb, route, "tril", info)
+
+
+def chol_fwd_fused(Sigma: torch.Tensor, Sdot: torch.Tensor, *, info: bool = False):
+    """Fused factorisation + forward mode (cd_chol_fwd_fused, fp64): in place, tril(Sigma) ->
+    L with Sigma = L L^T and tril(Sdot) -> L_dot, in one sweep.
+    Both tensors must already be column-major CUDA tensors (they are overwritten).
+    Returns (L, L_dot) [, info]."""
+    if not (is_colmajor(Sigma) and is_colmajor(Sdot)):
+        raise ValueError("chol_fwd_fused works in place: pass column-major tensors (see colmajor())")
+    A, Ad = Sigma, Sdot
+    if not (A.is_cuda and Ad.is_cuda) or A.shape != Ad.shape or A.dtype != Ad.dtype:
+        raise ValueError("chol_fwd_fused takes two CUDA tensors of the same shape and dtype")
+    r = _run(CD_OP_CHOL_FWD, A, Ad, None, "auto", "tril", info)
+    return (A, r[0], r[1]) if info else (A, r)
 
 
 def chol_host(op: str, L_host: torch.Tensor, A_host: torch.Tensor, *, nb=None, device=None) -> torch.Tensor:

@@ -37,6 +37,7 @@
 #include "symbolic_cta.cuh"
 #include "panel_rev.cuh"
 #include "panel_fwd.cuh"
+#include "chol_diag.cuh"
 #include "gemm_fwd_sk.cuh"
 
 namespace cd {
@@ -973,6 +974,9 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pf.Yws = Yws;
     pf.Fws = Fws;
     pf.Dc = Dc;
+    pf.T0 = A;
+    pf.single = 0;
+    pf.skip3 = 0;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
     void* args[] = {&pf};
     const double wf = w;
@@ -996,6 +1000,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
       fp.part = skpart;
       fp.cnt = cnt;
+      fp.chol = 0;
       c.pre(CD_PROF_SYMM, 2.0 * double(p) * w * (2.0 * q + w) * double(batch));
       k_fwd_sk<<<fp.G, LL_THREADS, FS_SMEM, c.st>>>(fp, tm);
       c.launched();
@@ -1011,6 +1016,133 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     c.pre(CD_PROF_OTHER, 0.0);
     k_diag_info<double><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
     c.launched();
+  }
+}
+
+// ------------------------------------------------------------------ fused factorisation + forward
+// chol_blocked and chol_blocked_fwd accumulated in one
+// sweep: in: tril(A) = Sigma, tril(Adot) = Sigma_dot; out: L, Ldot.
+// fp64, nb = 128, TMA-describable operands.  Per panel J = [j, k):
+//   k_panel_fwd  [phase 0: previous panel's Cdot <- W D^{-T}; phases 1-2: D <- D - tril(R R^T)]
+//   k_chol_diag  D <- chol_unblocked(D) on chip, D^{-1}
+//   k_fwd_sk     C <- C - B R^T                                  (factorisation mode)
+//   k_panel_fwd  [phase 0: C <- C D^{-T}; phases 1-3: Ddot -= tril(Rdot R^T + R Rdot^T), Eq. 8]
+//   k_fwd_sk     W = Cdot - [Bdot B C][R Rdot Dc]^T
+static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad, int* info) {
+  const int nblk = nblocks(n, nb);
+  double* Dinv = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * nb * nb));
+  double* part = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
+  double* Yws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
+  double* Fws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
+  double* Dc = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 132 * 128));
+  double* skpart = static_cast<double*>(c.take(sizeof(double) * size_t(c.sms) * 2 * LL_TILE));
+  int* cnt = static_cast<int*>(c.take(sizeof(int) * size_t(batch) * nblk));
+  if (c.plan || !c.ok()) return;
+  FSMaps tmf, tmc;
+  memset(&tmf, 0, sizeof(tmf));
+  tmf.batched = batch > 1 ? 1 : 0;
+  {
+    int sh = 0;
+    const double* Ab = static_cast<const double*>(A.base) + A.off;
+    const double* Adb = static_cast<const double*>(Ad.base) + Ad.off;
+    const bool ok = make_tmap(&tmf.adot, &sh, Adb, n, n, Ad.ld, Ad.stride, batch, FS_PITCH, LL_BK) &&
+                    make_tmap(&tmf.l, &sh, Ab, n, n, A.ld, A.stride, batch, FS_PITCH, LL_BK) &&
+                    make_tmap(&tmf.dc, &sh, Dc, 132, 128, 132, 132 * 128, batch, FS_PITCH, LL_BK);
+    if (!ok) {
+      c.err = CD_ERR_CUDA;
+      snprintf(g_cuda_err, sizeof(g_cuda_err), "cuTensorMapEncodeTiled failed for the fused sweep");
+      return;
+    }
+  }
+  tmc = tmf;  // factorisation mode reads only the `l` map
+  c.err = note_cuda(cudaMemsetAsync(cnt, 0, sizeof(int) * size_t(batch) * nblk, c.st));
+  if (info && c.ok()) c.err = note_cuda(cudaMemsetAsync(info, 0, sizeof(int) * size_t(batch), c.st));
+  set_smem(k_fwd_sk, FS_SMEM);
+  set_smem(k_panel_fwd, PR_SMEM);
+  const size_t dsm = dmma_cta_smem((nb + 7) / 8);
+  set_smem(k_chol_diag<double>, dsm);
+  const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
+  auto panel = [&](PanelFwdParams& pf, double flops) {
+    void* args[] = {&pf};
+    c.pre(CD_PROF_PANEL, flops * double(batch));
+    c.err = note_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_panel_fwd), dim3(grid),
+                                                  dim3(PR_THREADS), args, PR_SMEM, c.st));
+    c.launched();
+  };
+  auto sk = [&](int j, int w, int k, int p, int q, int chol, const FSMaps& tm, Opnd D) {
+    FSParams fp;
+    fp.A = D;
+    fp.n = n, fp.k = k, fp.j = j, fp.w = w, fp.q = q;
+    fp.m = (p + 127) / 128;
+    fp.KT = chol ? q / LL_BK : (2 * q + w + LL_BK - 1) / LL_BK;
+    fp.total = batch * int64_t(fp.m) * fp.KT;
+    if (fp.total >= (int64_t(1) << 31) || w != 128) {
+      c.err = CD_ERR_UNSUPPORTED;
+      return;
+    }
+    fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
+    fp.part = skpart;
+    fp.cnt = cnt;
+    fp.chol = chol;
+    c.pre(CD_PROF_SYMM, 2.0 * double(p) * w * double(chol ? q : 2.0 * q + w) * double(batch));
+    k_fwd_sk<<<fp.G, LL_THREADS, FS_SMEM, c.st>>>(fp, tm);
+    c.launched();
+  };
+  auto base_params = [&](PanelFwdParams& pf) {
+    memset(&pf, 0, sizeof(pf));
+    pf.dstride = int64_t(nblk) * nb * nb;
+    pf.dld = nb;
+    pf.n = n;
+    pf.batch = batch;
+    pf.part = part;
+    pf.Yws = Yws;
+    pf.Fws = Fws;
+    pf.Dc = Dc;
+  };
+  int j_prev = 0, k_prev = 0, p_prev = 0;
+  for (int qb = 0; qb < nblk && c.ok(); ++qb) {
+    int j, w;
+    block_range(n, nb, false, qb, j, w);
+    const int k = j + w, p = n - k, q = j;
+    if (qb > 0) {  // previous panel's forward solve; D <- D - tril(R R^T)
+      PanelFwdParams pf;
+      base_params(pf);
+      pf.A = A;
+      pf.L = A;
+      pf.T0 = Ad;
+      pf.Dinv = Dinv + int64_t(qb) * nb * nb;
+      pf.Dinv_prev = p_prev > 0 ? Dinv + int64_t(qb - 1) * nb * nb : nullptr;
+      pf.j_prev = j_prev, pf.k_prev = k_prev, pf.tiles_prev = (p_prev + 127) / 128;
+      pf.j = j, pf.w = w;
+      pf.kchunks = q / 128;
+      pf.single = 1;
+      pf.skip3 = 1;
+      panel(pf, double(p_prev) * 128 * 129 + double(w) * (w + 1) * q);
+    }
+    // D <- chol_unblocked(D), D^{-1}
+    c.pre(CD_PROF_SWEEP, (double(w) * w * w / 3.0 + double(w) * w * w / 3.0) * double(batch));
+    k_chol_diag<double><<<dim3(1, unsigned(batch)), DC_THREADS, dsm, c.st>>>(
+        w, sub(A, j, j), Dinv + int64_t(qb) * nb * nb, nb, int64_t(nblk) * nb * nb, j, info);
+    c.launched();
+    if (p > 0 && q > 0) sk(j, w, k, p, q, 1, tmc, A);  // C <- C - B R^T
+    {  // C <- C D^{-T}; the forward panel (Ddot update, Eq. 8)
+      PanelFwdParams pf;
+      base_params(pf);
+      pf.A = Ad;
+      pf.L = A;
+      pf.T0 = A;
+      pf.Dinv = Dinv + int64_t(qb) * nb * nb;
+      pf.Dinv_prev = p > 0 ? Dinv + int64_t(qb) * nb * nb : nullptr;
+      pf.j_prev = j, pf.k_prev = k, pf.tiles_prev = (p + 127) / 128;
+      pf.j = j, pf.w = w;
+      pf.kchunks = q / 128;
+      pf.single = 0;
+      pf.skip3 = 0;
+      const double wf = w;
+      panel(pf, double(p) * w * (w + 1) + 2.0 * wf * (wf + 1) * q + (4 * wf * wf * wf + 3 * wf * wf + 5 * wf) / 6);
+    }
+    if (p > 0 && c.ok()) sk(j, w, k, p, q, 0, tmf, Ad);  // W = Cdot - [Bdot B C][R Rdot Dc]^T
+    j_prev = j, k_prev = k, p_prev = p;
   }
 }
 
@@ -1036,6 +1168,62 @@ template <typename T>
 static void drive(Ctx& c, const Call& k) {
   const int n = int(k.n);
   if (n == 0 || k.batch == 0) return;
+  if (k.op == CD_OP_CHOL_FWD) {  // fused factorisation + forward (fp64; checked with the arguments)
+    if constexpr (sizeof(T) == 8) {
+      const Opnd Aop = k.L;  // tril(Sigma) in, L out (the call's first matrix, written)
+      const int nb = 128;
+      if (n <= DC_NMAX) {  // one block: factor on chip, then the on-chip forward sweep
+        double* Dinv = static_cast<double*>(c.take(sizeof(double) * size_t(k.batch) * n * n));
+        if (c.plan || !c.ok()) return;
+        if (k.info) c.err = note_cuda(cudaMemsetAsync(k.info, 0, sizeof(int) * size_t(k.batch), c.st));
+        const size_t dsm = dmma_cta_smem((n + 7) / 8);
+        set_smem(k_chol_diag<double>, dsm);
+        c.pre(CD_PROF_SWEEP, double(n) * n * n / 3.0 * double(k.batch));
+        k_chol_diag<double><<<dim3(1, unsigned(k.batch)), DC_THREADS, dsm, c.st>>>(n, Aop, Dinv, n, int64_t(n) * n, 0,
+                                                                                 k.info);
+        c.launched();
+        run_sweep_small<double>(c, false, n, k.batch, Aop, k.A, 0, null_opnd(), nullptr);
+        return;
+      }
+      if (g_tma_disabled) {
+        c.err = CD_ERR_UNSUPPORTED;
+        return;
+      }
+      const bool direct = !c.plan && (reinterpret_cast<uintptr_t>(static_cast<const double*>(Aop.base) + Aop.off) % 16) == 0 &&
+                          (reinterpret_cast<uintptr_t>(static_cast<const double*>(k.A.base) + k.A.off) % 16) == 0 &&
+                          Aop.ld % 2 == 0 && k.A.ld % 2 == 0 && !Aop.arr && !k.A.arr &&
+                          (k.batch == 1 || (Aop.stride % 2 == 0 && k.A.stride % 2 == 0));
+      if (direct) {
+        chol_fwd_fused(c, n, nb, k.batch, Aop, k.A, k.info);
+        return;
+      }
+      // odd ld / unaligned / pointer arrays: run on aligned workspace copies (ld even)
+      const int64_t ldw = n + (n & 1);
+      double* wA = static_cast<double*>(c.take(sizeof(double) * size_t(k.batch) * ldw * n));
+      double* wD = static_cast<double*>(c.take(sizeof(double) * size_t(k.batch) * ldw * n));
+      const Opnd OA = ws_opnd(wA, ldw * n, ldw), OD = ws_opnd(wD, ldw * n, ldw);
+      if (!c.plan && c.ok()) {  // lower triangles in
+        c.pre(CD_PROF_OTHER, 0.0);
+        k_copy_tril<double><<<grid_1d(int64_t(n) * n * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, Aop, OA);
+        c.launched();
+        c.pre(CD_PROF_OTHER, 0.0);
+        k_copy_tril<double><<<grid_1d(int64_t(n) * n * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, k.A, OD);
+        c.launched();
+      }
+      chol_fwd_fused(c, n, nb, k.batch, OA, OD, k.info);
+      if (!c.plan && c.ok()) {  // lower triangles back
+        c.pre(CD_PROF_OTHER, 0.0);
+        k_copy_tril<double><<<grid_1d(int64_t(n) * n * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, OA, Aop);
+        c.launched();
+        c.pre(CD_PROF_OTHER, 0.0);
+        k_copy_tril<double><<<grid_1d(int64_t(n) * n * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, OD, k.A);
+        c.launched();
+      }
+    } else {
+      c.err = CD_ERR_UNSUPPORTED;
+    }
+    return;
+  }
   if (k.o.route == CD_ROUTE_SYMBOLIC) {  // n <= SYM_NMAX (checked with the arguments)
     if (c.plan || !c.ok()) return;
     const int nblk = (n + 7) / 8;
@@ -1158,7 +1346,8 @@ static int check_common(cd_op op, int dt, int64_t n, int64_t ldl, int64_t lda, c
     if (opts->nb < 0) return -a_opts;
     if (opts->route < CD_ROUTE_AUTO || opts->route > CD_ROUTE_SYMBOLIC) return -a_opts;
     if (opts->out_mode < CD_OUT_TRIL || opts->out_mode > CD_OUT_GRAD) return -a_opts;
-    if (op == CD_OP_FWD && opts->out_mode != CD_OUT_TRIL) return -a_opts;
+    if (op != CD_OP_REV && opts->out_mode != CD_OUT_TRIL) return -a_opts;
+    if (op == CD_OP_CHOL_FWD && (opts->route == CD_ROUTE_SYMBOLIC || (opts->nb != 0 && opts->nb != 128))) return -a_opts;
     if (opts->flags != 0) return -a_opts;
   }
   return 0;
@@ -1244,6 +1433,22 @@ int cd_chol_fwd_batched(cd_dtype dt, int64_t n, const void* const* L_array, int6
                         int64_t ldadot, int64_t batch, const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
                         cd_stream_t stream) {
   return ptr_batched(CD_OP_FWD, dt, n, L_array, ldl, Adot_array, ldadot, batch, opts, ws, ws_bytes, d_info, stream);
+}
+
+int cd_chol_fwd_fused(cd_dtype dt, int64_t n, void* A, int64_t lda, void* Adot, int64_t ldadot, const cd_opts* opts,
+                      void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream) {
+  if (dt != CD_F64 && dt != CD_F32) return -1;
+  if (dt == CD_F32) return CD_ERR_UNSUPPORTED;
+  return strided(CD_OP_CHOL_FWD, dt, n, A, lda, 0, Adot, ldadot, 0, 1, opts, ws, ws_bytes, d_info, stream, true);
+}
+
+int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t lda, int64_t strideA, void* Adot,
+                                      int64_t ldadot, int64_t strideAdot, int64_t batch, const cd_opts* opts, void* ws,
+                                      size_t ws_bytes, int* d_info, cd_stream_t stream) {
+  if (dt != CD_F64 && dt != CD_F32) return -1;
+  if (dt == CD_F32) return CD_ERR_UNSUPPORTED;
+  return strided(CD_OP_CHOL_FWD, dt, n, A, lda, strideA, Adot, ldadot, strideAdot, batch, opts, ws, ws_bytes, d_info,
+                 stream, false);
 }
 
 size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts) {

@@ -6,7 +6,9 @@
 //   segment 0: A = Adot[k:n, 0:q]  (Bdot),  B(kk, c) = L[j + c, kk]      (R^T),     K = q
 //   segment 1: A = L[k:n, 0:q]     (B),     B(kk, c) = Adot[j + c, kk]   (Rdot^T),  K = q
 //   segment 2: A = L[k:n, j:k]     (C),     B(kk, c) = Dc[c, kk]         (Ddot^T),  K = w
-// written in place over Cdot.  The output is a narrow p x 128 panel with K = 2q + w, the
+// written in place over Cdot.  With `chol` set it is the factorisation's C <- C - B R^T
+// (chol_blocked) instead: segment 0 only, both operands from L.
+// The output is a narrow p x 128 panel with K = 2q + w, the
 // same shape as the left-looking reverse update, so it uses the same machinery as
 // k_symm_ll: TMA-fed DMMA with one producer and two consumer warpgroups (setmaxnreg), and
 // stream-K over batch x m x KT k-tiles with the deterministic last-arrival fixup instead
@@ -44,6 +46,8 @@ struct FSParams {
   int64_t total;     // batch * m * KT (< 2^31)
   double* part;      // [G][2][128*128]
   int* cnt;          // [batch * m], zero on entry, reset by the last CTA
+  int chol;          // factorisation mode (chol_blocked): W = C - B R^T, one
+                     // segment with A and B both from the `l` map (KT = q / 16)
 };
 
 __global__ void __launch_bounds__(LL_THREADS, 1) k_fwd_sk(const FSParams p, const __grid_constant__ FSMaps tm) {
@@ -83,9 +87,9 @@ __global__ void __launch_bounds__(LL_THREADS, 1) k_fwd_sk(const FSParams p, cons
         const int r0 = p.k + LL_BM * i;
         const CUtensorMap *am, *bm;
         int ac0, ac1, bc0, bc1;
-        if (kt < kq) {  // Bdot R^T
+        if (kt < kq) {  // Bdot R^T  (factorisation mode: B R^T)
           const int kk = kt * LL_BK;
-          am = &tm.adot, ac0 = r0, ac1 = kk;
+          am = p.chol ? &tm.l : &tm.adot, ac0 = r0, ac1 = kk;
           bm = &tm.l, bc0 = p.j, bc1 = kk;
         } else if (kt < 2 * kq) {  // B Rdot^T
           const int kk = (kt - kq) * LL_BK;

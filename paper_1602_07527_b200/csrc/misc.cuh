@@ -35,6 +35,19 @@ __global__ void k_copy(int M, int N, int64_t batch, Opnd S, Opnd D) {
   }
 }
 
+// D(i, j) = S(i, j) for i >= j (lower triangles only), n x n per batch entry.
+template <typename T>
+__global__ void k_copy_tril(int n, int64_t batch, Opnd S, Opnd D) {
+  const int64_t nn = int64_t(n) * n, total = nn * batch;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(idx % n), c = int((idx / n) % n);
+    if (r < c) continue;
+    const int64_t b = idx / nn;
+    optr_w<T>(D, b)[r + int64_t(c) * D.ld] = optr<T>(S, b)[r + int64_t(c) * S.ld];
+  }
+}
+
 // S = tril(A) + tril(A)^T (diagonal doubled), dense n x n; or (clean=1) S = tril(A), upper 0.
 template <typename T>
 __global__ void k_sym2(int n, int64_t batch, Opnd A, Opnd S, int clean) {

@@ -36,6 +36,10 @@ struct PanelFwdParams {
   double* Yws;           // dense 128 x 128 per batch entry
   double* Fws;           // dense 128 x 128 per batch entry
   double* Dc;            // dense, ld 132, batch stride 132 * 128
+  // generalisations for the fused factorisation + forward sweep (chol_fwd_fused):
+  Opnd T0;               // phase-0 target matrix (W <- W D^{-T} in place); the forward sweep: A
+  int single;            // phase 1: one product R R^T (K = 128 per chunk) instead of both
+  int skip3;             // skip phase 3 (Eq. 8)
 };
 
 // acc (64 x 32 warp tiles of a 128 x 128 tile) += sum over K of A(m, kk) B(kk, c), K in
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       const int64_t b = u / p.tiles_prev;
       const int tl = int(u - b * p.tiles_prev);
       const int r0 = p.k_prev + 128 * tl;
-      double* Wt = optr_w<double>(p.A, b) + r0 + int64_t(p.j_prev) * p.A.ld;
+      double* Wt = optr_w<double>(p.T0, b) + r0 + int64_t(p.j_prev) * p.T0.ld;
       const double* Di = p.Dinv_prev + b * p.dstride;
       double acc[8][4][2];
 #pragma unroll
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
         for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
       pf_prod128(
           sm, 128,
-          [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.A.ld : nullptr; },
+          [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.T0.ld : nullptr; },
           [&](int kk, int c) -> const double* { return c >= kk ? Di + c + int64_t(kk) * p.dld : nullptr; },
           [&](int kc) { return kc * 16 > wn * 32 + 31; },  // D^{-T}(kk, c) = 0 for kk > c
           acc);
@@ -132,7 +136,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int r = wm * 64 + i * 8 + g, c = wn * 32 + jj * 8 + 2 * t + e;
-            if (r0 + r < p.n) Wt[r + int64_t(c) * p.A.ld] = acc[i][jj][e];
+            if (r0 + r < p.n) Wt[r + int64_t(c) * p.T0.ld] = acc[i][jj][e];
           }
     }
     __threadfence();
@@ -145,13 +149,13 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       const int tl = int(bt - b * p.tiles_prev);
       const int ti = int(u & 15) >> 2, tj = int(u & 3);
       const int r0 = p.k_prev + 128 * tl + 32 * ti, c0 = 32 * tj;
-      const double* Wt = optr<double>(p.A, b) + r0 + int64_t(p.j_prev) * p.A.ld;  // rows r0.., panel cols
+      const double* Wt = optr<double>(p.T0, b) + r0 + int64_t(p.j_prev) * p.T0.ld;  // rows r0.., panel cols
       const double* Di = p.Dinv_prev + b * p.dstride;
       // write target: column-group tj of the same rows; the 4 column groups of a row group
       // read all of W's columns, so results go to the Yws-like staging slot first
       double* st = p.part + u * int64_t(32 * 32);
       pr_tile32(
-          sm, [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.A.ld : nullptr; },
+          sm, [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.T0.ld : nullptr; },
           [&](int kk, int n) -> const double* {
             const int cc = c0 + n;
             return cc >= kk ? Di + cc + int64_t(kk) * p.dld : nullptr;  // D^{-T}(kk, cc) = Dinv(cc, kk)
@@ -166,11 +170,11 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       const int tl = int(bt - b * p.tiles_prev);
       const int ti = int(u & 15) >> 2, tj = int(u & 3);
       const int r0 = p.k_prev + 128 * tl + 32 * ti, c0 = 32 * tj;
-      double* Wt = optr_w<double>(p.A, b) + r0 + int64_t(p.j_prev + c0) * p.A.ld;
+      double* Wt = optr_w<double>(p.T0, b) + r0 + int64_t(p.j_prev + c0) * p.T0.ld;
       const double* st = p.part + u * int64_t(32 * 32);
       for (int e = tid; e < 32 * 32; e += PR_THREADS) {
         const int m = e & 31, n = e >> 5;
-        if (r0 + m < p.n) Wt[m + int64_t(n) * p.A.ld] = __ldcg(st + e);
+        if (r0 + m < p.n) Wt[m + int64_t(n) * p.T0.ld] = __ldcg(st + e);
       }
     }
     __threadfence();
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
       pf_prod128(
-          sm, 256,
+          sm, p.single ? 128 : 256,
           [&](int m, int kk) -> const double* {
             if (m >= w) return nullptr;
             return kk < 128 ? Ad + m + int64_t(kk) * p.A.ld : Lr + m + int64_t(kk - 128) * p.L.ld;
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       double* slot = p.part + bk * int64_t(128 * 128);
       // kk < 128 -> Rdot(a, kk) R(c, kk); kk >= 128 -> R(a, kk') Rdot(c, kk')
       pr_tile32k(
-          sm, 256,
+          sm, p.single ? 128 : 256,
           [&](int m, int kk) -> const double* {
             const int a = a0 + m;
             if (a >= w) return nullptr;
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   }
 
   // ---------------- phase 3: Ldot_D = D Phi(D^{-1} Ddot_sym D^{-T})  (Eq. 8) ----------------
-  const int64_t u3 = p.batch * 16;
+  const int64_t u3 = p.skip3 ? 0 : p.batch * 16;
   // 3a: Y = D^{-1} X,  X(r, c) = Ddot(max, min)
   for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
     const int64_t b = u >> 4;

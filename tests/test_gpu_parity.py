@@ -228,3 +228,30 @@ def test_symbolic_route_upper_never_read_and_limits():
     L, Lb, _ = synthetic.draw(65, 4)
     with pytest.raises(cd.CholdiffError):
         cd.chol_rev(to_dev(L), to_dev(Lb), route="symbolic")
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 128, 129, 300, 517, 1024])
+def test_chol_fwd_fused(n):
+    # factorisation (oracle chol_unblocked PAPER.md:437-445)
+    # and forward mode accumulated in one sweep
+    B = 2 if n <= 300 or n == 1024 else 1
+    L, _, Sd = synthetic.draw_batch(n, B, seed=900 + n, sdot=True)
+    Sig = np.einsum("bij,bkj->bik", L, L)  # Sigma = L L^T
+    Lref = np.stack([oracle.chol(Sig[b]) for b in range(B)])
+    Fref = oracle_fwd(Lref, Sd)
+    A = to_dev(synthetic.poison_upper(Sig) if B == 1 else Sig)
+    Ad = to_dev(np.tril(Sd))
+    Lo, Fo = cd.chol_fwd_fused(A, Ad)
+    assert nerr(to_host(Lo), Lref) < TOL64
+    assert nerr(to_host(Fo), Fref) < TOL64
+    if B == 1:
+        assert np.all(np.isnan(to_host(Lo)[0][np.triu_indices(n, 1)]))
+
+
+def test_chol_fwd_fused_reports_indefinite():
+    n = 300
+    L, _, Sd = synthetic.draw(n, 5, sdot=True)
+    Sig = L @ L.T
+    Sig[200, 200] = -1.0  # not positive definite from pivot 201 on at the latest
+    _, _, info = cd.chol_fwd_fused(to_dev(Sig), to_dev(np.tril(Sd)), info=True)
+    assert 0 < int(info.cpu()[0]) <= 201

@@ -27,12 +27,15 @@ def main():
     a = ap.parse_args()
     dt = torch.float64 if a.dtype == "f64" else torch.float32
     if a.batch == 1:
-        L, Lb, Sd = synthetic.draw(a.n, 0, sdot=a.case == "fwd")
+        L, Lb, Sd = synthetic.draw(a.n, 0, sdot=a.case in ("fwd", "fused"))
     else:
-        L, Lb, Sd = synthetic.draw_batch(a.n, a.batch, seed=0, sdot=a.case == "fwd")
+        L, Lb, Sd = synthetic.draw_batch(a.n, a.batch, seed=0, sdot=a.case in ("fwd", "fused"))
     to = lambda m: torch.from_numpy(synthetic.to_colmajor(m)).to(dt).cuda().transpose(-1, -2)  # noqa: E731
     Ld = to(L)
-    A0 = to(Lb if a.case != "fwd" else np.tril(Sd))
+    A0 = to(Lb if a.case not in ("fwd", "fused") else np.tril(Sd))
+    if a.case == "fused":
+        S = Ld @ Ld.transpose(-1, -2)  # Sigma = L L^T on the device
+        S = S.transpose(-1, -2).contiguous().transpose(-1, -2)
     for nb in a.nb:
         ts = []
         for i in range(a.reps + 2):
@@ -40,7 +43,9 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
-            if a.case == "fwd":
+            if a.case == "fused":  # Sigma in A0's slot is replaced by a copy of L L^T
+                cd.chol_fwd_fused(S.clone(), A)
+            elif a.case == "fwd":
                 cd.chol_fwd(Ld, A, nb=nb)
             else:
                 cd.chol_rev(Ld, A, nb=nb)
