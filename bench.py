@@ -295,6 +295,26 @@ def bench_single_rev(args, dist: Dist):
                       "unit": "GFLOP/s", "frac_of_fp64_peak": round(fwd_flops(n) / (fw * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                       "steps": args.fwd_steps}
 
+    # ---- factorisation + forward mode fused in one sweep (Sigma = L L^T as input)
+    if args.fused_steps > 0:
+        S0 = (Ld @ Ld.transpose(0, 1)).transpose(0, 1).contiguous().transpose(0, 1)  # column-major Sigma
+        Sw = torch.empty_like(S0).transpose(0, 1).contiguous().transpose(0, 1)
+
+        def ustep():
+            cd.chol_fwd_fused(Sw, A)
+
+        def urestore():
+            Sw.copy_(S0)
+            A.copy_(A0)
+
+        ums = timed_steps(ustep, urestore, args.fused_steps, 1, dist, stream)
+        uw = dist.max(statistics.mean(ums))
+        ufl = n ** 3 / 3 + fwd_flops(n)
+        out["chol_fwd_fused"] = {"workload": f"cd_chol_fwd_fused fp64 N={n}: Sigma -> L and Sigma_dot -> L_dot in one sweep",
+                                 "ms_per_step": round(uw, 3), "value": round(ufl / (uw * 1e-3) / 1e9, 2),
+                                 "unit": "GFLOP/s (N^3/3 factorisation + fwd(N))", "steps": args.fused_steps}
+        del S0, Sw
+
     # ---- e2e through the host-buffer C-ABI call
     if args.e2e_steps > 0:
         pin_L = torch.from_numpy(Lcm).pin_memory().transpose(0, 1)
@@ -608,6 +628,7 @@ def main():
     ap.add_argument("--steps-batched", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--fwd-steps", type=int, default=2, help="timed chol_fwd steps at the same N (0 = skip)")
+    ap.add_argument("--fused-steps", type=int, default=2, help="timed chol_fwd_fused steps at the same N (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-cols", type=int, default=1024)
     ap.add_argument("--no-cpu", action="store_true")
