@@ -729,6 +729,7 @@ static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, 
 //                                               S = Dbar + Dbar^T kept per block for later M tiles
 // Requires fp64, nb = 128 and TMA-describable Abar / L (16-byte aligned, even ld).
 static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
+static int64_t g_ll_pieces = getenv("CD_LL_PIECES") ? atoi(getenv("CD_LL_PIECES")) : 8;
 static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DEBUG_PANEL_SKIP")) : 0;
 
 static int panel_occupancy() {
@@ -805,7 +806,11 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       lp.m = p / LL_BM;
       lp.nblk = nblk;
       lp.total = batch * int64_t(lp.m) * LL_KT_PER_BLK * lp.m;
-      lp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, lp.total / LL_KT_PER_BLK)));
+      // CTAs: at most ~PIECES pieces per output tile -- the last-arriving CTA sums all pieces
+      // of a tile alone, so with few tiles more CTAs cost more in the fixup than they save
+      const int64_t pieces = g_ll_pieces;
+      lp.G = int(std::max<int64_t>(1, std::min<int64_t>({int64_t(c.sms), lp.total / LL_KT_PER_BLK,
+                                                         pieces * batch * int64_t(lp.m)})));
       lp.part = llpart;
       lp.cnt = cnt;
       c.pre(CD_PROF_SYMM, 2.0 * double(p) * p * w * double(batch));
