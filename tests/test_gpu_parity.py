@@ -255,3 +255,25 @@ def test_chol_fwd_fused_reports_indefinite():
     Sig[200, 200] = -1.0  # not positive definite from pivot 201 on at the latest
     _, _, info = cd.chol_fwd_fused(to_dev(Sig), to_dev(np.tril(Sd)), info=True)
     assert 0 < int(info.cpu()[0]) <= 201
+
+
+@pytest.mark.parametrize("n,B", [(1100, 1), (2048, 1), (300, 3)])
+def test_f32_blocked_sizes(n, B):
+    # fp32 blocked paths (tf32 tcgen05 GEMMs, fp64-arithmetic diagonal blocks) beyond the
+    # batched configs: single large matrices with a ragged block and a batch of mid-size ones
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=31 + n, sdot=True)
+    L, Lb, Sd = fp32_round(L, Lb, Sd)
+    r = cd.chol_rev(to_dev(L, torch.float32), to_dev(Lb, torch.float32))
+    assert nerr(to_host(r), oracle_rev(L, Lb)) < TOL32
+    f = cd.chol_fwd(to_dev(L, torch.float32), to_dev(np.tril(Sd), torch.float32))
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL32
+
+
+@pytest.mark.parametrize("n", [2048, 2500])
+def test_f64_blocked_larger(n):
+    # several hundred stream-K pieces and panel steps, ragged last block (2500), fused paths
+    L, Lb, Sd = synthetic.draw(n, 55 + n, sdot=True)
+    r = cd.chol_rev(to_dev(L), to_dev(Lb))
+    assert nerr(to_host(r), oracle.chol_rev(L, Lb)) < TOL64
+    f = cd.chol_fwd(to_dev(L), to_dev(np.tril(Sd)))
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
