@@ -277,3 +277,55 @@ def test_f64_blocked_larger(n):
     assert nerr(to_host(r), oracle.chol_rev(L, Lb)) < TOL64
     f = cd.chol_fwd(to_dev(L), to_dev(np.tril(Sd)))
     assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
+
+
+def _guarded(m: np.ndarray, dtype, pad: int, gap: int):
+    """Column-major device copy of (B, n, n) `m` inside a larger buffer: `pad` guard rows below
+    each column (ld = n + pad) and `gap` guard columns between matrices (batch stride
+    (n + gap) * ld), all guard cells NaN.  Returns (view, underlying buffer, guard mask)."""
+    B, n = m.shape[0], m.shape[-1]
+    ld = n + pad
+    buf = np.full((B, n + gap, ld), np.nan)  # [b][column][row]
+    buf[:, :n, :n] = np.swapaxes(m, -1, -2)
+    guard = np.ones_like(buf, dtype=bool)
+    guard[:, :n, :n] = False
+    t = torch.from_numpy(buf).to(dtype).cuda()
+    view = t[:, :n, :n].transpose(-1, -2)  # logical (B, n, n), strides (ld*(n+gap), 1, ld)
+    return view, t, guard
+
+
+@pytest.mark.parametrize("n,B,dt", [(32, 9, torch.float64), (24, 5, torch.float64), (64, 4, torch.float64),
+                                    (300, 2, torch.float64), (129, 2, torch.float64), (300, 2, torch.float32),
+                                    (512, 2, torch.float32)])
+def test_no_writes_outside_the_matrices(n, B, dt):
+    # every path writes only inside tril of its matrices: NaN guard rows (ld > n) and guard
+    # columns between batch entries (stride > n * ld) must come back untouched
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=3 + n, sdot=True)
+    if dt == torch.float32:
+        L, Lb, Sd = fp32_round(L, Lb, Sd)
+    for op, src, ref in (("rev", Lb, oracle_rev(L, Lb)), ("fwd", np.tril(Sd), oracle_fwd(L, Sd))):
+        Lv, _, _ = _guarded(L, dt, 2, 3)
+        Av, Abuf, guard = _guarded(src, dt, 2, 3)
+        out = cd.chol_rev(Lv, Av) if op == "rev" else cd.chol_fwd(Lv, Av)
+        assert out.data_ptr() == Av.data_ptr()
+        assert nerr(to_host(out), ref) < (TOL64 if dt == torch.float64 else TOL32)
+        assert np.all(np.isnan(to_host(Abuf)[guard]))
+
+
+@pytest.mark.parametrize("n,B", [(40, 3), (300, 2)])
+def test_no_writes_outside_symbolic_and_fused(n, B):
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=8 + n, sdot=True)
+    if n <= 64:
+        Lv, _, _ = _guarded(L, torch.float64, 2, 3)
+        Av, Abuf, guard = _guarded(Lb, torch.float64, 2, 3)
+        out = cd.chol_rev(Lv, Av, route="symbolic")
+        assert nerr(to_host(out), oracle_rev(L, Lb)) < TOL64
+        assert np.all(np.isnan(to_host(Abuf)[guard]))
+    S = np.einsum("bij,bkj->bik", L, L)
+    Sv, Sbuf, g1 = _guarded(S, torch.float64, 2, 3)
+    Dv, Dbuf, g2 = _guarded(np.tril(Sd), torch.float64, 2, 3)
+    Lo, Fo = cd.chol_fwd_fused(Sv, Dv)
+    Lref = np.stack([oracle.chol(S[b]) for b in range(B)])
+    assert nerr(to_host(Lo), Lref) < TOL64
+    assert nerr(to_host(Fo), oracle_fwd(Lref, Sd)) < TOL64
+    assert np.all(np.isnan(to_host(Sbuf)[g1])) and np.all(np.isnan(to_host(Dbuf)[g2]))

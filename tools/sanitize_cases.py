@@ -1,0 +1,36 @@
+"""Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck /
+synccheck) runs (measurement / QA tool, not the product path)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1602_07527_b200 as cd  # noqa: E402
+import synthetic  # noqa: E402
+
+
+def dev(m, dt=torch.float64):
+    return torch.from_numpy(synthetic.to_colmajor(m)).to(dt).cuda().transpose(-1, -2)
+
+
+def main():
+    for n, B in ((300, 1), (300, 2), (32, 37), (24, 5), (64, 3), (517, 1)):
+        L, Lb, Sd = (synthetic.draw(n, n, sdot=True) if B == 1 else synthetic.draw_batch(n, B, seed=n, sdot=True))
+        cd.chol_rev(dev(L), dev(Lb))
+        cd.chol_fwd(dev(L), dev(np.tril(Sd)))
+        cd.chol_rev(dev(L, torch.float32), dev(Lb, torch.float32))
+        cd.chol_fwd(dev(L, torch.float32), dev(np.tril(Sd), torch.float32))
+        if n <= 64:
+            cd.chol_rev(dev(L), dev(Lb), route="symbolic")
+        S = np.einsum("...ij,...kj->...ik", L, L)
+        cd.chol_fwd_fused(dev(S), dev(np.tril(Sd)))
+    torch.cuda.synchronize()
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()
