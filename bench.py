@@ -527,7 +527,10 @@ def bench_small_configs(args, dist: Dist):
                                                 dist, stream)))
     tf = dist.max(statistics.median(timed_steps(lambda: cd.chol_fwd(Ld, F), lambda: F.copy_(F0), 10, args.warmup,
                                                 dist, stream)))
+    ts = dist.max(statistics.median(timed_steps(lambda: cd.chol_rev(Ld, A, route="symbolic"), lambda: A.copy_(A0),
+                                                5, args.warmup, dist, stream)))
     out["n1024"] = {"workload": "configs[1]: fp64 N=1024, seed 0", "rev_ms": round(tr, 3), "fwd_ms": round(tf, 3),
+                    "rev_symbolic_route_ms": round(ts, 3),
                     "rev_gflops": round(rev_flops(1024) / (tr * 1e-3) / 1e9, 1),
                     "fwd_gflops": round(fwd_flops(1024) / (tf * 1e-3) / 1e9, 1)}
     # configs[3]: 1024 x N=512 fp32, reverse + forward per step, sharded by matrix

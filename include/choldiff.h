@@ -74,8 +74,9 @@ typedef enum { CD_OP_REV = 0, CD_OP_FWD = 1, CD_OP_CHOL_FWD = 2 } cd_op;
 /* Route (the symbolic result may be preferable for small
  * matrices).  AUTO = ALGORITHMIC (measured faster on B200 at every size); ALGORITHMIC =
  * the paper's unblocked/blocked sweeps; SYMBOLIC = Eq. 10
- * (reverse) / Eq. 8 (forward) on the whole matrix,
- * one CTA per matrix, offered for n <= 64; larger n return CD_ERR_UNSUPPORTED. */
+ * (reverse) / Eq. 8 (forward) on the whole matrix:
+ * one CTA per matrix for n <= 64, blocked triangular solves on the GEMM kernels above
+ * (about 6x the sweep's flops; for measurement). */
 typedef enum { CD_ROUTE_AUTO = 0, CD_ROUTE_ALGORITHMIC = 1, CD_ROUTE_SYMBOLIC = 2 } cd_route;
 
 /* Reverse-mode output convention (reading c1):

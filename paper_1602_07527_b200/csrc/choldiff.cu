@@ -1151,6 +1151,83 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
   }
 }
 
+// ------------------------------------------------------------------ symbolic route, large n
+// Eqs. 10 / 8 on the whole matrix for n > 64:
+//   reverse  X = P + P^T, P = Phi(L^T Lbar);  Y = L^{-T} X L^{-1};  tril(Sigmabar) = Phi(Y)
+//   forward  Y = L^{-1} Sigmadot L^{-T};  Ldot = L Phi(Y)
+// Products are the library's GEMM kernels on clean (upper-zero) triangular copies; the two
+// triangular solves are blocked over 128-column blocks with the diagonal-block inverses
+// (k_trinv_dmma) -- the "Level 3 ... solving a triangular system" of PAPER.md:634-636.
+// About 4 n^3 flops against the sweep's 2 n^3 / 3: offered for measurement (north star (d),
+// "worth measuring against the blocked sweep"); AUTO never picks it.
+template <typename T>
+static void symbolic_large(Ctx& c, int n, int64_t batch, bool rev, Opnd L, Opnd A, int out_mode, T* part) {
+  const int nb = 128, nblk = nblocks(n, nb);
+  const int64_t nn = int64_t(n) * n;
+  T* Lc = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nn));
+  T* X = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nn));
+  T* Z = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nn));
+  T* Dinv = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nblk * nb * nb));
+  if (c.plan || !c.ok()) return;
+  const Opnd OL = ws_opnd(Lc, nn, n), OX = ws_opnd(X, nn, n), OZ = ws_opnd(Z, nn, n);
+  auto elem = [&](Opnd S, Opnd D, int mode) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_sym_elem<T><<<grid_1d(nn * batch, 256, c.sms), 256, 0, c.st>>>(n, batch, S, D, mode);
+    c.launched();
+  };
+  elem(L, OL, 0);  // clean tril(L)
+  run_trinv<T>(c, n, nb, false, batch, L, Dinv);
+  auto dinv = [&](int qb) { return ws_opnd(Dinv + int64_t(qb) * nb * nb, int64_t(nblk) * nb * nb, nb); };
+  if (rev) {
+    elem(A, OZ, 0);  // clean tril(Lbar)
+    Gemm<T>(c, n, n, 1, 0, batch).seg(OL, OZ, n).run(null_opnd(), OX, 1.0, 0.0, 0, part);  // L^T Lbar
+    elem(OX, OZ, 1);  // Z = Phi(P) + Phi(P)^T
+    // right solve W = Z L^{-1}: column blocks right to left, W[:, J] = (Z[:, J] - W[:, k:n] L[k:n, J]) D_J^{-1}
+    for (int qb = nblk - 1; qb >= 0 && c.ok(); --qb) {
+      int j, w;
+      block_range(n, nb, false, qb, j, w);
+      const int k = j + w;
+      if (k < n) Gemm<T>(c, n, w, 0, 0, batch).seg(sub(OZ, 0, k), sub(OL, k, j), n - k).run(sub(OZ, 0, j), sub(OZ, 0, j), -1.0, 1.0, 0, part);
+      Gemm<T>(c, n, w, 0, 0, batch).seg(sub(OZ, 0, j), dinv(qb), w).run(null_opnd(), sub(OZ, 0, j), 1.0, 0.0, 0, part);
+    }
+    // left solve Y = L^{-T} W: row blocks bottom to top, Y[J, :] = D_J^{-T} (W[J, :] - L[k:n, J]^T Y[k:n, :])
+    for (int qb = nblk - 1; qb >= 0 && c.ok(); --qb) {
+      int j, w;
+      block_range(n, nb, false, qb, j, w);
+      const int k = j + w;
+      if (k < n) Gemm<T>(c, w, n, 1, 0, batch).seg(sub(OL, k, j), sub(OZ, k, 0), n - k).run(sub(OZ, j, 0), sub(OZ, j, 0), -1.0, 1.0, 0, part);
+      Gemm<T>(c, w, n, 1, 0, batch).seg(dinv(qb), sub(OZ, j, 0), w).run(null_opnd(), sub(OZ, j, 0), 1.0, 0.0, 0, part);
+    }
+    elem(OZ, A, 4);  // tril(Sigmabar) = Phi(Y)
+    if (out_mode != CD_OUT_TRIL && c.ok()) {
+      c.pre(CD_PROF_OTHER, 0.0);
+      k_out_mode<T><<<grid_1d(nn * batch, 256, c.sms), 256, 0, c.st>>>(n, batch, A, out_mode);
+      c.launched();
+    }
+  } else {
+    elem(A, OZ, 2);  // X = Sigmadot, symmetric
+    // left solve Y = L^{-1} X: row blocks top to bottom, Y[J, :] = D_J^{-1} (X[J, :] - L[J, 0:j] Y[0:j, :])
+    for (int qb = 0; qb < nblk && c.ok(); ++qb) {
+      int j, w;
+      block_range(n, nb, false, qb, j, w);
+      if (j > 0) Gemm<T>(c, w, n, 0, 0, batch).seg(sub(OL, j, 0), OZ, j).run(sub(OZ, j, 0), sub(OZ, j, 0), -1.0, 1.0, 0, part);
+      Gemm<T>(c, w, n, 0, 0, batch).seg(dinv(qb), sub(OZ, j, 0), w).run(null_opnd(), sub(OZ, j, 0), 1.0, 0.0, 0, part);
+    }
+    // right solve Z = Y L^{-T}: column blocks left to right, Z[:, J] = (Y[:, J] - Z[:, 0:j] L[J, 0:j]^T) D_J^{-T}
+    for (int qb = 0; qb < nblk && c.ok(); ++qb) {
+      int j, w;
+      block_range(n, nb, false, qb, j, w);
+      if (j > 0) Gemm<T>(c, n, w, 0, 1, batch).seg(OZ, sub(OL, j, 0), j).run(sub(OZ, 0, j), sub(OZ, 0, j), -1.0, 1.0, 0, part);
+      Gemm<T>(c, n, w, 0, 1, batch).seg(sub(OZ, 0, j), dinv(qb), w).run(null_opnd(), sub(OZ, 0, j), 1.0, 0.0, 0, part);
+    }
+    elem(OZ, OX, 3);  // F = Phi(Z), clean
+    Gemm<T>(c, n, n, 0, 0, batch).seg(OL, OX, n).run(null_opnd(), OZ, 1.0, 0.0, 0, part);  // Ldot = L F
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_copy_tril<T><<<grid_1d(nn * batch, 256, c.sms), 256, 0, c.st>>>(n, batch, OZ, A);
+    c.launched();
+  }
+}
+
 // ------------------------------------------------------------------ top-level
 struct Call {
   cd_op op;
@@ -1229,7 +1306,40 @@ static void drive(Ctx& c, const Call& k) {
     }
     return;
   }
-  if (k.o.route == CD_ROUTE_SYMBOLIC) {  // n <= SYM_NMAX (checked with the arguments)
+  if (k.o.route == CD_ROUTE_SYMBOLIC && n > SYM_NMAX) {
+    double* part = static_cast<double*>(c.take(sizeof(double) * size_t(PART_TILES) * G_BM * G_BN));
+    if constexpr (sizeof(T) == 8) {
+      symbolic_large<double>(c, n, k.batch, k.op == CD_OP_REV, k.L, k.A, k.o.out_mode, part);
+    } else {
+      // fp32: four chained tf32 products would miss the 1e-4 gate -- run the route in fp64
+      // on converted copies (it is offered for measurement, not speed)
+      const int64_t nn = int64_t(n) * n;
+      double* L64 = static_cast<double*>(c.take(sizeof(double) * size_t(k.batch) * nn));
+      double* A64 = static_cast<double*>(c.take(sizeof(double) * size_t(k.batch) * nn));
+      const Opnd OL = ws_opnd(L64, nn, n), OA = ws_opnd(A64, nn, n);
+      if (!c.plan && c.ok()) {
+        c.pre(CD_PROF_OTHER, 0.0);
+        k_convert_tril<float, double><<<grid_1d(nn * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, k.L, OL);
+        c.launched();
+        c.pre(CD_PROF_OTHER, 0.0);
+        k_convert_tril<float, double><<<grid_1d(nn * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, k.A, OA);
+        c.launched();
+      }
+      symbolic_large<double>(c, n, k.batch, k.op == CD_OP_REV, OL, OA, CD_OUT_TRIL, part);
+      if (!c.plan && c.ok()) {
+        c.pre(CD_PROF_OTHER, 0.0);
+        k_convert_tril<double, float><<<grid_1d(nn * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, OA, k.A);
+        c.launched();
+        if (k.op == CD_OP_REV && k.o.out_mode != CD_OUT_TRIL) {
+          c.pre(CD_PROF_OTHER, 0.0);
+          k_out_mode<float><<<grid_1d(nn * k.batch, 256, c.sms), 256, 0, c.st>>>(n, k.batch, k.A, k.o.out_mode);
+          c.launched();
+        }
+      }
+    }
+    return;
+  }
+  if (k.o.route == CD_ROUTE_SYMBOLIC) {  // n <= SYM_NMAX: one CTA per matrix
     if (c.plan || !c.ok()) return;
     const int nblk = (n + 7) / 8;
     const size_t smem = symbolic_smem(nblk);
@@ -1359,9 +1469,10 @@ static int check_common(cd_op op, int dt, int64_t n, int64_t ldl, int64_t lda, c
 }
 
 static int route_supported(const cd_opts& o, int64_t n) {
-  // the symbolic route (Eqs. 8 / 10 on the whole matrix) is offered for small matrices,
-  // where the paper recommends it; larger n use the blocked sweeps
-  if (o.route == CD_ROUTE_SYMBOLIC && n > SYM_NMAX) return CD_ERR_UNSUPPORTED;
+  // every route is available at every size: symbolic = k_symbolic_cta (n <= 64) or
+  // symbolic_large (blocked triangular solves); AUTO = the algorithmic sweeps
+  (void)o;
+  (void)n;
   return 0;
 }
 

@@ -86,6 +86,48 @@ __global__ void k_out_mode(int n, int64_t batch, Opnd A, int mode) {
   }
 }
 
+// Elementwise steps of the large-n symbolic route (dense n x n per batch entry):
+//   mode 0: D = tril(S), upper zero                       (clean triangular operand)
+//   mode 1: D = Phi(S) + Phi(S)^T, from tril(S)            (X = P + P^T; D != S)
+//   mode 2: D = symmetric from tril(S)                      (Sigma_dot read as symmetric)
+//   mode 3: D = Phi(S) (lower, diagonal halved, upper zero)
+//   mode 4: tril(D) = Phi(S) (lower only, D's upper untouched)
+template <typename T>
+__global__ void k_sym_elem(int n, int64_t batch, Opnd S, Opnd D, int mode) {
+  const int64_t nn = int64_t(n) * n, total = nn * batch;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(idx % n), c = int((idx / n) % n);
+    const int64_t b = idx / nn;
+    const T* s = optr<T>(S, b);
+    T* d = optr_w<T>(D, b);
+    const T lo = r >= c ? s[r + int64_t(c) * S.ld] : s[c + int64_t(r) * S.ld];  // tril(S)(max, min)
+    T v;
+    switch (mode) {
+      case 0: v = r >= c ? lo : T(0); break;
+      case 1: case 2: v = lo; break;                 // Phi(S)+Phi(S)^T has the diagonal of S
+      case 3: v = r > c ? lo : (r == c ? T(0.5) * lo : T(0)); break;
+      default:
+        if (r < c) continue;
+        v = r > c ? lo : T(0.5) * lo;
+    }
+    d[r + int64_t(c) * D.ld] = v;
+  }
+}
+
+// tril(D) = tril(S) converted between element types (n x n per batch entry)
+template <typename TS, typename TD>
+__global__ void k_convert_tril(int n, int64_t batch, Opnd S, Opnd D) {
+  const int64_t nn = int64_t(n) * n, total = nn * batch;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(idx % n), c = int((idx / n) % n);
+    if (r < c) continue;
+    const int64_t b = idx / nn;
+    optr_w<TD>(D, b)[r + int64_t(c) * D.ld] = TD(optr<TS>(S, b)[r + int64_t(c) * S.ld]);
+  }
+}
+
 // info[b] = first 1-based j with L[j-1, j-1] zero or non-finite, else 0.  One CTA per matrix.
 template <typename T>
 __global__ void k_diag_info(int n, Opnd Ld, int* __restrict__ info) {

@@ -89,7 +89,9 @@ def test_workspace_sizes():
     assert cd.workspace_size("rev", torch.float64, 1000, 1, nb=64) > 0
 
 
-def test_symbolic_route_unsupported_status():
-    # the symbolic route is offered for n <= 64 only (include/choldiff.h); larger n: CD_ERR_UNSUPPORTED
-    o = cd._Opts(0, 2, 0, 0)
-    assert _rev(65, 65, 65, opts=ctypes.byref(o)) == 2
+def test_symbolic_route_workspace():
+    # the large-n symbolic route needs dense scratch copies (3 n^2 + block inverses), the
+    # small-n one none
+    import torch
+    assert cd.workspace_size("rev", torch.float64, 64, 7, route="symbolic") == 0
+    assert cd.workspace_size("rev", torch.float64, 300, 1, route="symbolic") >= 3 * 300 * 300 * 8

@@ -225,9 +225,7 @@ def test_symbolic_route_upper_never_read_and_limits():
                               route="symbolic"))
     assert np.all(np.isnan(out[np.triu_indices(n, 1)]))
     assert nerr(out, oracle.chol_rev(L, Lb)) < TOL64
-    L, Lb, _ = synthetic.draw(65, 4)
-    with pytest.raises(cd.CholdiffError):
-        cd.chol_rev(to_dev(L), to_dev(Lb), route="symbolic")
+
 
 
 @pytest.mark.parametrize("n", [1, 7, 64, 128, 129, 300, 517, 1024])
@@ -329,3 +327,21 @@ def test_no_writes_outside_symbolic_and_fused(n, B):
     assert nerr(to_host(Lo), Lref) < TOL64
     assert nerr(to_host(Fo), oracle_fwd(Lref, Sd)) < TOL64
     assert np.all(np.isnan(to_host(Sbuf)[g1])) and np.all(np.isnan(to_host(Dbuf)[g2]))
+
+
+@pytest.mark.parametrize("n,B", [(65, 3), (200, 2), (300, 1), (517, 1)])
+def test_symbolic_route_large(n, B):
+    # Eqs. 10 / 8 on the whole matrix via blocked triangular solves
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=600 + n, sdot=True)
+    r = cd.chol_rev(to_dev(L), to_dev(Lb), route="symbolic")
+    assert nerr(to_host(r), oracle_rev(L, Lb)) < TOL64
+    f = cd.chol_fwd(to_dev(L), to_dev(np.tril(Sd)), route="symbolic")
+    assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL64
+    g = to_host(cd.chol_rev(to_dev(L), to_dev(Lb), route="symbolic", out="grad"))
+    g0 = to_host(cd.chol_rev(to_dev(L), to_dev(Lb), out="grad"))
+    assert np.abs(g - g0).max() / np.linalg.norm(g0.reshape(B, -1), axis=1).min() < TOL64
+    L32, Lb32, Sd32 = fp32_round(L, Lb, Sd)
+    r32 = cd.chol_rev(to_dev(L32, torch.float32), to_dev(Lb32, torch.float32), route="symbolic")
+    assert nerr(to_host(r32), oracle_rev(L32, Lb32)) < TOL32
+    f32 = cd.chol_fwd(to_dev(L32, torch.float32), to_dev(np.tril(Sd32), torch.float32), route="symbolic")
+    assert nerr(to_host(f32), oracle_fwd(L32, Sd32)) < TOL32
