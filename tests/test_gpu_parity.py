@@ -345,3 +345,29 @@ def test_symbolic_route_large(n, B):
     assert nerr(to_host(r32), oracle_rev(L32, Lb32)) < TOL32
     f32 = cd.chol_fwd(to_dev(L32, torch.float32), to_dev(np.tril(Sd32), torch.float32), route="symbolic")
     assert nerr(to_host(f32), oracle_fwd(L32, Sd32)) < TOL32
+
+
+@pytest.mark.parametrize("n,B,dt", [(64, 1, torch.float64), (32, 37, torch.float64), (300, 1, torch.float64),
+                                    (300, 2, torch.float32)])
+def test_cuda_graph_capture_and_replay(n, B, dt):
+    # the library enqueues only stream-ordered work (launches, memsets, event fork/join of its
+    # own streams), so a call can be captured once into a CUDA graph and replayed
+    L, Lb, _ = synthetic.draw_batch(n, B, seed=44 + n)
+    if dt == torch.float32:
+        L, Lb = fp32_round(L, Lb)
+    Ld, A0 = to_dev(L, dt), to_dev(Lb, dt)
+    A = A0.clone().transpose(-1, -2).contiguous().transpose(-1, -2)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        cd.chol_rev(Ld, A)  # warm-up outside capture (library streams, kernel attributes)
+    torch.cuda.current_stream().wait_stream(s)
+    A.copy_(A0)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cd.chol_rev(Ld, A)
+    for _ in range(3):
+        A.copy_(A0)
+        g.replay()
+    torch.cuda.synchronize()
+    assert nerr(to_host(A), oracle_rev(L, Lb)) < (TOL64 if dt == torch.float64 else TOL32)
