@@ -12,7 +12,7 @@
 // same shape as the left-looking reverse update, so it uses the same machinery as
 // k_symm_ll: TMA-fed DMMA with one producer and two consumer warpgroups (setmaxnreg), and
 // stream-K over batch x m x KT k-tiles with the deterministic last-arrival fixup instead
-// of split-K partials + a reduction launch.  Every operand tile is one TMA box of 132 x 16
+// of split-K partials + a reduction launch.  Every operand tile is one TMA box of 132 x BK
 // (the 4-row pad makes the shared-memory pitch 4 mod 16 doubles: conflict-free fragments):
 // A as As[k][m], B as Bs[k][c].
 #pragma once
@@ -41,7 +41,7 @@ struct FSParams {
   Opnd A;            // Adot, whole matrix (Cin and D of the output panel)
   int n, k, j, w, q;
   int m;             // output row tiles = ceil((n - k) / 128)
-  int KT;            // k-tiles per output tile = (2q + w) / 16
+  int KT;            // k-tiles per output tile = (2q + w) / BK
   int G;
   int64_t total;     // batch * m * KT (< 2^31)
   double* part;      // [G][2][128*128]

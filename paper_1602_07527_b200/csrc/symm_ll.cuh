@@ -25,7 +25,7 @@
 //     s >  i : T[s, i]ᵀ           read in place, transposed     (A tile "MK": As[m][k])
 //   B tile = L[k+128s+kk .., j:j+128] (Bs[n][k]).
 //
-// Work split: stream-K.  The batch * m tiles * 8m k-tiles are cut into G equal
+// Work split: stream-K.  The batch * m tiles * (128/BK)m k-tiles are cut into G equal
 // contiguous ranges, one per CTA (G <= #SMs, one CTA per SM).  A tile covered by one
 // CTA is written directly (Cin prefetched into the accumulators); a tile split across
 // CTAs has each piece stored to a partial slot, and the LAST arriving CTA (atomic
@@ -40,13 +40,21 @@
 
 namespace cd {
 
-constexpr int LL_BM = 128, LL_BN = 128, LL_BK = 16;
+// K step 32 x 3 stages (221 KB): half the per-stage barrier traffic of 16 x 5 at the same
+// bytes in flight (N=16384 reverse 94.3 -> 93.2 ms)
+#ifndef CD_LL_BK
+#define CD_LL_BK 32
+#endif
+#ifndef CD_LL_STAGES
+#define CD_LL_STAGES 3
+#endif
+constexpr int LL_BM = 128, LL_BN = 128, LL_BK = CD_LL_BK;
 constexpr int LL_KT_PER_BLK = 128 / LL_BK;  // k-tiles per 128-wide K block
-constexpr int LL_STAGES = 5;
+constexpr int LL_STAGES = CD_LL_STAGES;
 constexpr int LL_CONSUMERS = 8;                    // warps 0..7 (two warpgroups)
 constexpr int LL_THREADS = (LL_CONSUMERS + 4) * 32;  // + one producer warpgroup (warps 8..11)
 constexpr int LL_A_KM_PITCH = LL_BM + 4, LL_A_MK_PITCH = LL_BK + 4, LL_B_PITCH = LL_BK + 4;
-constexpr int LL_A_SIZE = LL_BM * (LL_BK + 4);  // max(16*132, 128*20) = 2560 doubles
+constexpr int LL_A_SIZE = LL_BM * (LL_BK + 4) > LL_BK * (LL_BM + 4) ? LL_BM * (LL_BK + 4) : LL_BK * (LL_BM + 4);
 constexpr int LL_B_SIZE = LL_BN * (LL_BK + 4);  // 2560
 constexpr uint32_t LL_BYTES_KM = uint32_t(LL_BK * (LL_BM + 4)) * 8u;  // 16896
 constexpr uint32_t LL_BYTES_MK = uint32_t(LL_BM * (LL_BK + 4)) * 8u;  // 20480
@@ -55,10 +63,10 @@ constexpr size_t LL_SMEM = size_t(LL_STAGES) * (LL_A_SIZE + LL_B_SIZE) * 8 + 2 *
 constexpr int LL_TILE = LL_BM * LL_BN;  // doubles per partial slot
 
 struct LLMaps {
-  CUtensorMap aN;  // Abar, box {132 rows, 16 cols}
-  CUtensorMap aT;  // Abar, box {20 rows, 128 cols}
-  CUtensorMap s;   // S workspace (132 x 128*nblk per batch), box {132, 16}
-  CUtensorMap l;   // L, box {20, 128}
+  CUtensorMap aN;  // Abar, box {132 rows, BK cols}
+  CUtensorMap aT;  // Abar, box {BK+4 rows, 128 cols}
+  CUtensorMap s;   // S workspace (132 x 128*nblk per batch), box {132, BK}
+  CUtensorMap l;   // L, box {BK+4, 128}
   int batched;
 };
 
@@ -68,7 +76,7 @@ struct LLParams {
   int m;           // output row tiles = (n - k) / 128
   int nblk;        // blocks of the reverse partition (S slot of the block at row r0: nblk - (n - r0)/128)
   int G;           // CTAs
-  int64_t total;   // batch * m * 8m k-tiles (< 2^31, checked by the host)
+  int64_t total;   // batch * m * (128/BK)m k-tiles (< 2^31, checked by the host)
   double* part;    // [G][2][128*128] partial slots
   int* cnt;        // [batch * m] arrival counters (zero on entry, reset by the last CTA)
 };
