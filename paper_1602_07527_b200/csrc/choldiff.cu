@@ -1378,7 +1378,10 @@ static void drive(Ctx& c, const Call& k) {
     if (!ll || c.plan) {
       // lookahead schedule needs a one-tile-wide block (in-place panel solve) and library streams
       T* part2 = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
-      LaStreams* ls = (!g_no_lookahead && nb <= G_BN) ? (c.plan ? reinterpret_cast<LaStreams*>(1) : la_streams()) : nullptr;
+      // (batches already fill the GPU: the lookahead's extra launches only cost there)
+      LaStreams* ls = (!g_no_lookahead && nb <= G_BN && k.batch == 1)
+                          ? (c.plan ? reinterpret_cast<LaStreams*>(1) : la_streams())
+                          : nullptr;
       if (ls) blocked_rev_la<T>(c, ls, n, nb, k.batch, k.L, k.A, k.info, part, part2);
       else blocked_rev<T>(c, n, nb, k.batch, k.L, k.A, k.info, part);
     }
