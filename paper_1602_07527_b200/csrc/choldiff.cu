@@ -730,6 +730,8 @@ static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, 
 // Requires fp64, nb = 128 and TMA-describable Abar / L (16-byte aligned, even ld).
 static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
 static int64_t g_ll_pieces = getenv("CD_LL_PIECES") ? atoi(getenv("CD_LL_PIECES")) : 8;
+// the SYMM moves into the panel kernel while its 32 x 32 output tiles number <= this x #SMs
+static int64_t g_symm_in_panel = getenv("CD_SYMM_IN_PANEL") ? atoi(getenv("CD_SYMM_IN_PANEL")) : 1;
 static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DEBUG_PANEL_SKIP")) : 0;
 
 static int panel_occupancy() {
@@ -799,7 +801,9 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     block_range(n, nb, true, qb, j, w);
     const int k = j + w, p = n - k;
     if (g_pipe) cudaStreamWaitEvent(c.st, ev_in[size_t(qb)], 0);
-    if (p > 0) {
+    // small trailing part: the SYMM runs as phase 0 of the panel kernel (one launch per step)
+    const bool symm_in_panel = p > 0 && batch * int64_t(p / LL_BM) * 16 <= int64_t(c.sms) * g_symm_in_panel;
+    if (p > 0 && !symm_in_panel) {
       LLParams lp;
       lp.A = A;
       lp.n = n, lp.k = k, lp.j = j, lp.w = w;
@@ -840,6 +844,10 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pp.s_stride = s_stride;
     pp.dbg_skip = g_dbg_panel_skip;
     pp.Wst = Wst;
+    pp.symm = symm_in_panel ? 1 : 0;
+    pp.Sall = Sall;
+    pp.s_blk = int64_t(LL_BM + 4) * LL_BM;
+    pp.nblk = nblk;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs
     void* args[] = {&pp};
     const double wf = w;

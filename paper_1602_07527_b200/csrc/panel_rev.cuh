@@ -56,6 +56,11 @@ struct PanelParams {
   int64_t s_stride;
   int dbg_skip;  // measurement only (CD_DEBUG_PANEL_SKIP): bit i skips phase i+1; results wrong
   double* Wst;   // small-panel phase 1 staging of W: [batch * tiles][128 * 128]
+  // phase 0 (small panels, instead of a k_symm_ll launch): Cbar -= (T + T^T) L[k:n, j:k]
+  int symm;              // 1: run phase 0
+  const double* Sall;    // S blocks (ld s_ld, block stride s_blk, batch stride s_stride) = diagonal tiles of M
+  int64_t s_blk;
+  int nblk;              // S slot of the block at row r0: nblk - (n - r0) / 128
 };
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
@@ -115,6 +120,42 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   const int wm = warp >> 2, wn = wm == 0 ? (warp & 3) : 3 - (warp & 3), g = lane >> 2, t = lane & 3;
   const int w = p.w;
   const int64_t units = p.batch * p.tiles;
+
+  // ---------------- phase 0 (small panels): Cbar -= M L[k:n, j:k], M = T + T^T ----------------
+  // The left-looking trailing update of symm_ll.cuh for panels with few row tiles, done here
+  // in 32 x 32 output tiles over the grid (K = p) instead of a separate stream-K launch:
+  // M(r, c) = T(r, c) below the diagonal blocks, T(c, r) above them, S on them.
+  if (p.symm && !(p.dbg_skip & 8)) {
+    const int64_t u0 = units * 16;
+    const int pk = p.n - p.k;
+    for (int64_t u = blockIdx.x; u < u0; u += gridDim.x) {
+      const int64_t bt = u >> 4;
+      const int64_t b = bt / p.tiles;
+      const int tl = int(bt - b * p.tiles);
+      const int ti = int(u & 15) >> 2, tj = int(u & 3);
+      const int r0 = p.k + 128 * tl + 32 * ti, c0 = 32 * tj;
+      const int rb = 128 * tl;  // row block (relative to k) of this output tile
+      const double* Ab = optr<double>(p.A, b);
+      const double* Lb = optr<double>(p.L, b) + p.k + int64_t(p.j) * p.L.ld;
+      const double* Sb = p.Sall + b * p.s_stride + int64_t(p.nblk - (p.n - (p.k + rb)) / 128) * p.s_blk;
+      double* Cb = optr_w<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;
+      pr_tile32k(
+          sm, pk,
+          [&](int m, int kk) -> const double* {  // M(r0 + m, k + kk)
+            const int r = r0 + m - p.k, cblk = kk & ~127;
+            if (cblk < rb) return Ab + (r0 + m) + int64_t(p.k + kk) * p.A.ld;        // T(r, c)
+            if (cblk > rb) return Ab + (p.k + kk) + int64_t(r0 + m) * p.A.ld;        // T(c, r)
+            return Sb + (r - rb) + int64_t(kk - rb) * p.s_ld;                         // S block
+          },
+          [&](int kk, int n) -> const double* { return c0 + n < w ? Lb + kk + int64_t(c0 + n) * p.L.ld : nullptr; },
+          [&](int m, int n, double v) {
+            if (c0 + n < w) Cb[m + int64_t(c0 + n) * p.A.ld] -= v;
+          });
+    }
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+  }
+
   // few tiles (early steps): split every tile's work into 32 x 32 tiles over the grid --
   // 1a: W = Cbar D^{-1} (16 tiles per 128-row tile, staged), grid sync, 1b: the lower
   // 32 x 32 tiles of P_t = W^T C (K = the tile's 128 rows) and W copied back in place
