@@ -289,7 +289,28 @@ static bool make_tmap_f32_sw128(CUtensorMap* map, const void* p, int64_t rows, i
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 map without swizzle (TMA epilogue of the tcgen05 kernel: 128 x 32 column-major chunks)
+static bool make_tmap_f32_plain(CUtensorMap* map, const void* p, int64_t rows, int64_t cols, int64_t ld,
+                                int64_t bstride, int64_t batch, int box0, int box1) {
+  auto enc = tmap_encoder();
+  if (!enc || rows <= 0 || cols <= 0) return false;
+  if (reinterpret_cast<uintptr_t>(p) % 16) return false;
+  if ((ld * 4) % 16 || (batch > 1 && (bstride * 4) % 16)) return false;
+  cuuint64_t dims[3] = {cuuint64_t(rows), cuuint64_t(cols), cuuint64_t(std::max<int64_t>(batch, 1))};
+  cuuint64_t strides[2] = {cuuint64_t(ld * 4), cuuint64_t(std::max<int64_t>(bstride, 1) * 4)};
+  cuuint32_t box[3] = {cuuint32_t(box0), cuuint32_t(box1), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const cuuint32_t rank = batch > 1 ? 3 : 2;
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
+// TMA epilogue of the tcgen05 GEMM (gemm_tc32.cuh, EPI = 1): on unless CD_TC_EPI=0;
+// CD_TC_EPI_STAGES = operand ring depth with it (2: two CTAs per SM, 3: one)
+static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
+static int g_tc_epi_stages = getenv("CD_TC_EPI_STAGES") ? atoi(getenv("CD_TC_EPI_STAGES")) : 3;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
 
 // ------------------------------------------------------------------ GEMM launcher
@@ -425,12 +446,48 @@ struct Gemm {
                                : make_tmap_f32_sw128(&tm.b[s], pb, p.N, sg.K, sg.B.ld, sg.B.stride, p.batch, 32, 32, true);
       if (!okA || !okB) return false;
     }
-    auto kern = k_gemm_tc32<A_, B_>;
-    set_smem(kern, TC_SMEM);
-    // persistent: a grid of (up to) 2 CTAs per SM loops over the units (TMEM: 2 x 256 columns)
     const int64_t units = int64_t(grid.x) * grid.y * grid.z;
-    const unsigned g = unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(c.sms) * 2)));
-    kern<<<g, TCP_THREADS, TC_SMEM, c.st>>>(p, tm);
+    if (units >= (int64_t(1) << 31)) return false;  // the kernel decodes units in 32 bits
+    TcEpiMaps em;
+    memset(&em, 0, sizeof(em));
+    if (tc_epi_maps(em)) {
+      if (g_tc_epi_stages == 3) return launch_tc32_k<A_, B_, 1, 3>(units, tm, em);
+      return launch_tc32_k<A_, B_, 1, 2>(units, tm, em);
+    }
+    return launch_tc32_k<A_, B_, 0, TC_STAGES>(units, tm, em);
+  }
+  // TMA epilogue eligibility (see gemm_tc32.cuh): one split, plain strided D / Cin, 16-byte
+  // aligned, and a tril mask only for the in-place update
+  bool tc_epi_maps(TcEpiMaps& em) {
+    if (!g_tc_epi || p.splits != 1 || p.D.arr) return false;
+    const bool has_cin = p.beta != 0.0;
+    const bool inplace = p.Cin.base == p.D.base && !p.Cin.arr && p.Cin.off == p.D.off && p.Cin.ld == p.D.ld &&
+                         p.Cin.stride == p.D.stride;
+    if (p.tril && !(has_cin && inplace)) return false;
+    if (has_cin && p.Cin.arr) return false;
+    const float* pd = static_cast<const float*>(p.D.base) + p.D.off;
+    if (!make_tmap_f32_plain(&em.d, pd, p.M, p.N, p.D.ld, p.D.stride, p.batch, 128, 32)) return false;
+    if (has_cin) {
+      const float* pc = static_cast<const float*>(p.Cin.base) + p.Cin.off;
+      if (!make_tmap_f32_plain(&em.cin, pc, p.M, p.N, p.Cin.ld, p.Cin.stride, p.batch, 128, 32)) return false;
+    }
+    return true;
+  }
+  template <int A_, int B_, int EPI, int STG>
+  bool launch_tc32_k(int64_t units, const TmaMaps& tm, const TcEpiMaps& em) {
+    auto kern = k_gemm_tc32<A_, B_, EPI, STG>;
+    constexpr size_t smem = tc_smem(STG, EPI);
+    static int occ = 0;  // per instantiation
+    if (!occ) {
+      set_smem(kern, smem);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, tcp_threads(EPI), smem) != cudaSuccess || occ < 1)
+        occ = 1;
+      occ = std::min(occ, 2);  // TMEM: 2 x 256 columns per CTA
+    }
+    set_smem(kern, smem);
+    // persistent: a grid of (up to) occ CTAs per SM loops over the units
+    const unsigned g = unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(c.sms) * occ)));
+    kern<<<g, tcp_threads(EPI), smem, c.st>>>(p, tm, em);
     c.launched();
     return true;
   }

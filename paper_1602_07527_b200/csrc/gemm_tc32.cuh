@@ -37,7 +37,35 @@ constexpr int TC_STAGES = CD_TC_STAGES;
 constexpr int TC_THREADS = 128;
 constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32;
 constexpr uint32_t TC_STAGE_BYTES = (TC_BM + TC_BN) * TC_BK * 4;  // 32 KB
-constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + 1024 + 256;  // + barriers, TMEM slot
+constexpr uint32_t TC_ECHUNK_BYTES = TC_BM * 32 * 4;              // one 128 x 32 epilogue chunk, 16 KB
+#ifndef CD_TC_ESLOTS
+#define CD_TC_ESLOTS 6
+#endif
+constexpr int TC_ESLOTS = CD_TC_ESLOTS;  // TMA epilogue chunk slots (Cin prefetch depth ESLOTS - 1)
+// stages + (TMA epilogue) chunk slots + barriers / TMEM slot
+__host__ __device__ constexpr size_t tc_smem(int stages, int epi) {
+  return size_t(stages) * TC_STAGE_BYTES + (epi ? TC_ESLOTS * TC_ECHUNK_BYTES : 0) + 1024 + 256;
+}
+constexpr size_t TC_SMEM = tc_smem(TC_STAGES, 0);
+
+// output / Cin maps of the TMA epilogue: fp32, box {128 rows, 32 cols}, no swizzle (so the
+// staged chunk is column-major 128 x 32 and thread = row reads / writes it conflict-free)
+struct TcEpiMaps {
+  CUtensorMap d, cin;
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 
 // shared-memory matrix descriptor; layout 2 = SWIZZLE_128B (K-major operands),
 // 1 = SWIZZLE_128B_BASE32B (MN-major tf32 operands: the only MN-major layout for tf32)
@@ -87,31 +115,49 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
 // so TMEM allocation, barrier setup and the epilogue of one unit overlap the next unit's
 // loads and MMAs (the batched updates are tens of thousands of short-K tiles).
 constexpr int TCP_THREADS = 192;
+// EPI = 1 adds warp 6: the epilogue's TMA warp (Cin prefetch + output stores)
+__host__ __device__ constexpr int tcp_threads(int epi) { return epi ? 224 : 192; }
 
-template <int TA, int TB>
-__global__ void __launch_bounds__(TCP_THREADS, CD_TC_MINB) k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm) {
+// EPI = 0: registers epilogue (Cin loaded per thread-row, direct stores).
+// EPI = 1: TMA epilogue -- Cin chunks (128 x 32) are prefetched by TMA into two smem slots one
+//          chunks ahead (TC_ESLOTS slots), the result is written back into the slot and stored by TMA
+//          (cp.async.bulk.tensor ... bulk_group), so several Cin loads and output stores are
+//          in flight per CTA (a one-chunk prefetch left the batched updates latency-bound at
+//          ~1.7 TB/s).  Host-side conditions: splits == 1,
+//          D (and Cin) TMA-describable, and a tril mask only for the in-place update
+//          (masked elements are written back unchanged).
+// STG = depth of the operand ring.
+template <int TA, int TB, int EPI, int STG>
+__global__ void __launch_bounds__(tcp_threads(EPI), CD_TC_MINB)
+    k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm, const __grid_constant__ TcEpiMaps em) {
+  constexpr int TC_STAGES = STG;
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_tc) + 1023) & ~uintptr_t(1023));
   unsigned char* As = base;                                   // stages of A (16 KB each)
   unsigned char* Bs = base + TC_STAGES * (TC_BM * TC_BK * 4);  // stages of B (16 KB each)
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + TC_STAGES * TC_STAGE_BYTES);
+  unsigned char* Es = base + TC_STAGES * TC_STAGE_BYTES;      // EPI: 128 x 32 chunk slots
+  uint64_t* full = reinterpret_cast<uint64_t*>(Es + (EPI ? TC_ESLOTS * TC_ECHUNK_BYTES : 0));
   uint64_t* empty = full + TC_STAGES;
   uint64_t* accf = empty + TC_STAGES;  // [2] accumulator ready
   uint64_t* acce = accf + 2;           // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  uint64_t* cinf = acce + 2;           // [TC_ESLOTS] EPI: slot s ready (Cin landed / slot free)
+  uint64_t* donef = cinf + TC_ESLOTS;  // [TC_ESLOTS] EPI: chunk in slot s computed (4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(donef + TC_ESLOTS);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mt = (p.M + TC_BM - 1) / TC_BM, ntl = (p.N + TC_BN - 1) / TC_BN;
   const int64_t units = int64_t(mt) * ntl * p.batch * p.splits;
+  // (32-bit: the host guarantees units < 2^31; 64-bit division is a long subroutine)
   auto decode = [&](int64_t u, int& m0, int& n0, int64_t& b, int& split) {
-    const int64_t tmn = int64_t(mt) * ntl;
-    const int64_t zb = u / tmn;
-    const int r = int(u - zb * tmn);
-    m0 = (r % mt) * TC_BM;
-    n0 = (r / mt) * TC_BN;
-    split = int(zb % p.splits);
-    b = zb / p.splits;
+    const unsigned tmn = unsigned(mt) * unsigned(ntl);
+    const unsigned uu = unsigned(u);
+    const unsigned zb = uu / tmn;
+    const unsigned r = uu - zb * tmn;
+    m0 = int(r % unsigned(mt)) * TC_BM;
+    n0 = int(r / unsigned(mt)) * TC_BN;
+    split = int(zb % unsigned(p.splits));
+    b = int64_t(zb / unsigned(p.splits));
   };
   auto krange = [&](int split, int& kt0, int& nkt) {
     kt0 = split * p.kt_per_split;
@@ -127,6 +173,10 @@ __global__ void __launch_bounds__(TCP_THREADS, CD_TC_MINB) k_gemm_tc32(const Gem
     mbar_init(&accf[1], 1);
     mbar_init(&acce[0], 4);
     mbar_init(&acce[1], 4);
+    for (int s = 0; s < TC_ESLOTS; ++s) {
+      mbar_init(&cinf[s], 1);
+      mbar_init(&donef[s], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {  // TMEM: 2 x 128 columns x 128 lanes of fp32 accumulators
@@ -219,6 +269,104 @@ __global__ void __launch_bounds__(TCP_THREADS, CD_TC_MINB) k_gemm_tc32(const Gem
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          smem_u32(&accf[buf]))
                      : "memory");
+      }
+    }
+  } else if (EPI == 1 && warp == 6) {
+    // ---------------- epilogue TMA warp (lane 0): Cin prefetch and output stores ----------------
+    if (lane == 0) {
+      const bool has_cin = p.beta != 0.0;
+      auto nchunks = [&](int n0) { return (min(TC_BN, p.N - n0) + 31) / 32; };
+      // ready cursor: chunk lg (chunk lc of unit lu) gets slot lg % ESLOTS -- loaded from Cin,
+      // or just released when there is no Cin
+      int64_t lu = blockIdx.x;
+      int lc = 0, lg = 0;
+      auto ready_next = [&]() {
+        if (lu >= units) return;
+        int m0, n0, split;
+        int64_t b;
+        decode(lu, m0, n0, b, split);
+        const int slot = lg % TC_ESLOTS;
+        if (has_cin) {
+          mbar_expect_tx(&cinf[slot], TC_ECHUNK_BYTES);
+          if (tm.batched) tma_load_3d(Es + slot * TC_ECHUNK_BYTES, &em.cin, m0, n0 + 32 * lc, int(b), &cinf[slot]);
+          else tma_load_2d(Es + slot * TC_ECHUNK_BYTES, &em.cin, m0, n0 + 32 * lc, &cinf[slot]);
+        } else {
+          mbar_arrive(&cinf[slot]);
+        }
+        ++lg;
+        if (++lc == nchunks(n0)) lc = 0, lu += gridDim.x;
+      };
+      for (int k = 0; k < TC_ESLOTS - 1; ++k) ready_next();
+      int g = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int m0, n0, split;
+        int64_t b;
+        decode(u, m0, n0, b, split);
+        const int nch = nchunks(n0);
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int slot = g % TC_ESLOTS;
+          tc_wait(&donef[slot], (g / TC_ESLOTS) & 1);
+          unsigned char* E = Es + slot * TC_ECHUNK_BYTES;
+          if (tm.batched) tma_store_3d(&em.d, E, m0, n0 + 32 * c, int(b));
+          else tma_store_2d(&em.d, E, m0, n0 + 32 * c);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          // chunk g + ESLOTS - 1 takes the slot of chunk g - 1 once that store has read it
+          asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+          ready_next();
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    }
+  } else if (EPI == 1) {
+    // ---------------- TMA epilogue: warps 2..5, thread = accumulator row ----------------
+    const int q = warp & 3;
+    const int rr = q * 32 + lane;  // row within the tile (TMEM lane)
+    const float alpha = float(p.alpha), beta = float(p.beta);
+    const bool has_cin = p.beta != 0.0;
+    auto nchunks = [&](int n0) { return (min(TC_BN, p.N - n0) + 31) / 32; };
+    int i = 0, g = 0;  // unit counter, global chunk counter
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      int m0, n0, split, kt0, nkt;
+      int64_t b;
+      decode(u, m0, n0, b, split);
+      krange(split, kt0, nkt);
+      const int buf = i & 1;
+      tc_wait(&accf[buf], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int nch = nchunks(n0);
+      const int r = m0 + rr;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int slot = g % TC_ESLOTS;
+        float* E = reinterpret_cast<float*>(Es + slot * TC_ECHUNK_BYTES);
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * TC_BN + 32 * c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (c + 1 == nch) {  // accumulator drained: the MMA issuer may reuse the buffer
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acce[buf]);
+        }
+        tc_wait(&cinf[slot], (g / TC_ESLOTS) & 1);  // Cin landed / slot released
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const int col = n0 + 32 * c + jj;
+          const float acc = nkt > 0 ? __uint_as_float(v[jj]) : 0.f;
+          const float ci = has_cin ? E[jj * 128 + rr] : 0.f;
+          const bool keep = p.tril && !(r + p.tril - 1 >= col);
+          E[jj * 128 + rr] = keep ? ci : alpha * acc + beta * ci;
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&donef[slot]);
       }
     }
   } else {
