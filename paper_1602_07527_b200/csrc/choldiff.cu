@@ -308,9 +308,9 @@ static bool make_tmap_f32_plain(CUtensorMap* map, const void* p, int64_t rows, i
 
 static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
 // TMA epilogue of the tcgen05 GEMM (gemm_tc32.cuh, EPI = 1): on unless CD_TC_EPI=0;
-// CD_TC_EPI_STAGES = operand ring depth with it (2: two CTAs per SM, 3: one)
+// CD_TC_EPI_STAGES = operand ring depth with it (2: two CTAs per SM; 3, 4: one)
 static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
-static int g_tc_epi_stages = getenv("CD_TC_EPI_STAGES") ? atoi(getenv("CD_TC_EPI_STAGES")) : 3;
+static int g_tc_epi_stages = getenv("CD_TC_EPI_STAGES") ? atoi(getenv("CD_TC_EPI_STAGES")) : 4;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
 
 // ------------------------------------------------------------------ GEMM launcher
@@ -451,6 +451,7 @@ struct Gemm {
     TcEpiMaps em;
     memset(&em, 0, sizeof(em));
     if (tc_epi_maps(em)) {
+      if (g_tc_epi_stages == 4) return launch_tc32_k<A_, B_, 1, 4>(units, tm, em);
       if (g_tc_epi_stages == 3) return launch_tc32_k<A_, B_, 1, 3>(units, tm, em);
       return launch_tc32_k<A_, B_, 1, 2>(units, tm, em);
     }

@@ -5,19 +5,22 @@
 //   warp 0 lane 0 : TMA producer (cp.async.bulk.tensor, mbarrier complete_tx)
 //   warp 1 lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128 N=128 K=8;
 //                   tcgen05.commit releases each smem stage and finally the accumulator)
-//   warps 0..3    : epilogue (tcgen05.ld 32x32b: thread = accumulator row; coalesced
-//                   column-major stores, alpha/beta, tril mask, split-K partials)
+//   warps 2..5    : epilogue (tcgen05.ld 32x32b: thread = accumulator row)
+//   warp 6        : (EPI = 1) the epilogue's TMA warp: prefetches Cin chunks into smem slots
+//                   and stores finished chunks with cp.async.bulk.tensor
+//   last 8 warps  : round each landed operand stage to tf32 in place (cvt.rna) -- SURVEY c11:
+//                   the MMA would otherwise truncate the low 13 mantissa bits (biased error;
+//                   rounding cut the batched N = 512 error 4.3e-5 -> 1.1e-5 against the 1e-4 gate)
 //
-// Two stages and three CTAs per SM (TMEM 3 x 128 columns): the batched updates are
-// many short-K tiles, so overlapping one CTA's epilogue with another's main loop beats
-// a deeper pipeline (1024 x 512 fp32 batched: rev 5.26 -> 4.28 ms vs 4 stages).
+// Persistent grid (one CTA per SM with the TMA epilogue), two TMEM accumulator buffers so one
+// unit's epilogue overlaps the next unit's loads and MMAs.
 //
 // Operand layouts: K-contiguous operands use the K-major SW128 canonical layout (one
 // TMA box of 32 x 128, 128-byte swizzle); M/N-contiguous operands use the MN-major
 // SW128-with-32-byte-atoms layout (four TMA boxes of 32 x 32, SWIZZLE_128B_ATOM_32B),
-// the only MN-major layout tcgen05 accepts for tf32.  TF32 operands (10-bit mantissa, products accumulated in fp32):
-// DESIGN.md §6 gives the error budget against the 1e-4 gate.  Same GemmParams
-// semantics as k_gemm / k_gemm_tma.
+// the only MN-major layout tcgen05 accepts for tf32.  TF32 operands (10-bit mantissa, products
+// accumulated in fp32): DESIGN.md §6 gives the error budget against the 1e-4 gate.  Same
+// GemmParams semantics as k_gemm / k_gemm_tma.
 #pragma once
 #include <cuda.h>
 
@@ -89,6 +92,15 @@ __host__ __device__ constexpr uint32_t tc_idesc(int a_mn_major, int b_mn_major) 
          | ((128u >> 4) << 24);          // M >> 4
 }
 
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ float4 tf32_rna4(float4 v) {
+  return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+}
+
 __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
   // bounded wait: a protocol error becomes a trap instead of a hung GPU
   uint32_t spins = 0;
@@ -115,8 +127,14 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
 // so TMEM allocation, barrier setup and the epilogue of one unit overlap the next unit's
 // loads and MMAs (the batched updates are tens of thousands of short-K tiles).
 constexpr int TCP_THREADS = 192;
-// EPI = 1 adds warp 6: the epilogue's TMA warp (Cin prefetch + output stores)
-__host__ __device__ constexpr int tcp_threads(int epi) { return epi ? 224 : 192; }
+// EPI = 1 adds warp 6: the epilogue's TMA warp (Cin prefetch + output stores).  The last four
+// warps round every operand stage to tf32 in place (cvt.rna) before the MMA reads it.
+#ifndef CD_TC_CONVW
+#define CD_TC_CONVW 8
+#endif
+constexpr int TC_CONVW = CD_TC_CONVW;  // rounding warps
+__host__ __device__ constexpr int tc_conv_warp0(int epi) { return epi ? 7 : 6; }
+__host__ __device__ constexpr int tcp_threads(int epi) { return (tc_conv_warp0(epi) + TC_CONVW) * 32; }
 
 // EPI = 0: registers epilogue (Cin loaded per thread-row, direct stores).
 // EPI = 1: TMA epilogue -- Cin chunks (128 x 32) are prefetched by TMA into two smem slots one
@@ -128,7 +146,7 @@ __host__ __device__ constexpr int tcp_threads(int epi) { return epi ? 224 : 192;
 //          (masked elements are written back unchanged).
 // STG = depth of the operand ring.
 template <int TA, int TB, int EPI, int STG>
-__global__ void __launch_bounds__(tcp_threads(EPI), CD_TC_MINB)
+__global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
     k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm, const __grid_constant__ TcEpiMaps em) {
   constexpr int TC_STAGES = STG;
   extern __shared__ __align__(1024) unsigned char smem_tc[];
@@ -143,7 +161,8 @@ __global__ void __launch_bounds__(tcp_threads(EPI), CD_TC_MINB)
   uint64_t* acce = accf + 2;           // [2] accumulator drained
   uint64_t* cinf = acce + 2;           // [TC_ESLOTS] EPI: slot s ready (Cin landed / slot free)
   uint64_t* donef = cinf + TC_ESLOTS;  // [TC_ESLOTS] EPI: chunk in slot s computed (4 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(donef + TC_ESLOTS);
+  uint64_t* conv = donef + TC_ESLOTS;  // [TC_STAGES] stage s rounded to tf32 (TC_CONVW warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + TC_STAGES);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mt = (p.M + TC_BM - 1) / TC_BM, ntl = (p.N + TC_BN - 1) / TC_BN;
@@ -168,6 +187,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), CD_TC_MINB)
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], TC_CONVW);
     }
     mbar_init(&accf[0], 1);
     mbar_init(&accf[1], 1);
@@ -245,7 +265,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), CD_TC_MINB)
         const uint32_t acc_t = tmem + uint32_t(buf * TC_BN);
         for (int kk = 0; kk < nkt; ++kk, ++it) {
           const int s = it % TC_STAGES;
-          tc_wait(&full[s], (it / TC_STAGES) & 1);
+          tc_wait(&conv[s], (it / TC_STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t sa = smem_u32(As + s * (TC_BM * TC_BK * 4));
           const uint32_t sb = smem_u32(Bs + s * (TC_BN * TC_BK * 4));
@@ -269,6 +289,34 @@ __global__ void __launch_bounds__(tcp_threads(EPI), CD_TC_MINB)
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          smem_u32(&accf[buf]))
                      : "memory");
+      }
+    }
+  } else if (warp >= tc_conv_warp0(EPI)) {
+    // ---------------- tf32 rounding of each landed stage (round to nearest,
+    // ties away -- cvt.rna -- instead of the MMA's silent truncation of the low 13 bits) --------
+    const int ct = tid - tc_conv_warp0(EPI) * 32;
+    int it = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int m0, n0, split, kt0, nkt;
+      int64_t b;
+      decode(u, m0, n0, b, split);
+      krange(split, kt0, nkt);
+      for (int kk = 0; kk < nkt; ++kk, ++it) {
+        const int s = it % TC_STAGES;
+        tc_wait(&full[s], (it / TC_STAGES) & 1);
+        float4* a4 = reinterpret_cast<float4*>(As + s * (TC_BM * TC_BK * 4));
+        float4* b4 = reinterpret_cast<float4*>(Bs + s * (TC_BN * TC_BK * 4));
+#pragma unroll 4
+        for (int e = ct; e < TC_BM * TC_BK / 4; e += TC_CONVW * 32) {
+          float4 x = a4[e], y = b4[e];
+          x = tf32_rna4(x);
+          y = tf32_rna4(y);
+          a4[e] = x;
+          b4[e] = y;
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
       }
     }
   } else if (EPI == 1 && warp == 6) {

@@ -40,6 +40,9 @@ __device__ __forceinline__ int tat(int NBLK, int i, int m) {
   return tile_base(NBLK, i >> 3, m >> 3) + t8(i & 7, m & 7);
 }
 
+#ifndef CD_DC_MINB
+#define CD_DC_MINB 4  // 64 registers: 4 CTAs per SM at n <= 64 (batched fp32 diagonal blocks: -5 %)
+#endif
 constexpr int DC_NMAX = 128;  // largest n (and diagonal block) handled on chip
 constexpr int DC_WARPS = 8;
 constexpr int DC_THREADS = DC_WARPS * 32;
@@ -141,7 +144,7 @@ __device__ __forceinline__ void dc_store(int NBLK, TIO* __restrict__ g, int64_t 
 
 // ============================================================================ reverse
 template <typename TIO>
-__global__ void __launch_bounds__(DC_THREADS, 1)
+__global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
     k_rev_dmma_cta(int n, Opnd Ld, Opnd Ad, int out_mode, Opnd Sd, int* __restrict__ info) {
   const int NBLK = (n + 7) >> 3;
   const int NP = 8 * NBLK;
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
 // Optionally writes a clean dense copy of tril(Ldot) (upper zero) to Dd, the operand of
 // Cdot <- (Cdot - C Ddot^T) D^{-T} in the blocked driver.
 template <typename TIO>
-__global__ void __launch_bounds__(DC_THREADS, 1)
+__global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
     k_fwd_dmma_cta(int n, Opnd Ld, Opnd Ad, Opnd Dd, int* __restrict__ info) {
   const int NBLK = (n + 7) >> 3;
   const int NP = 8 * NBLK;
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
 // Dinv[b][q] = tril(L[j0:j0+w, j0:j0+w])^{-1}, dense w x w (ld = ldi), upper zero;
 // grid = (blocks, batch); block ranges as block_range (misc.cuh).
 template <typename TIO>
-__global__ void __launch_bounds__(DC_THREADS, 1)
+__global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
     k_trinv_dmma(int n, int nb, int reverse, Opnd Ld, TIO* __restrict__ Dinv, int64_t ldi, int64_t stride_blk) {
   const int NBLK = (nb + 7) >> 3;  // tiling of the widest block; shorter blocks are padded
   const int NP = 8 * NBLK;

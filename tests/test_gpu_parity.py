@@ -267,6 +267,18 @@ def test_f32_blocked_sizes(n, B):
     assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL32
 
 
+@pytest.mark.parametrize("nb", [64, 128])
+def test_f32_tf32_rounded_operands(nb):
+    # the tcgen05 GEMM rounds its operands to tf32 (cvt.rna) instead of letting the
+    # MMA truncate them: config-4-shaped matrices (n = 512) land near 1e-5 (truncation: 4.3e-5)
+    L, Lb, Sd = synthetic.draw_batch(512, 4, seed=543, sdot=True)
+    L, Lb, Sd = fp32_round(L, Lb, Sd)
+    r = cd.chol_rev(to_dev(L, torch.float32), to_dev(Lb, torch.float32), nb=nb)
+    assert nerr(to_host(r), np.stack([oracle.chol_rev(L[b], Lb[b]) for b in range(4)])) < 2.5e-5
+    f = cd.chol_fwd(to_dev(L, torch.float32), to_dev(np.tril(Sd), torch.float32), nb=nb)
+    assert nerr(to_host(f), np.stack([oracle.chol_fwd(L[b], Sd[b]) for b in range(4)])) < 2.5e-5
+
+
 @pytest.mark.parametrize("n", [2048, 2500])
 def test_f64_blocked_larger(n):
     # several hundred stream-K pieces and panel steps, ragged last block (2500), fused paths
