@@ -162,6 +162,35 @@ int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t l
                                       const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
                                       cd_stream_t stream);
 
+/* ---- Distributed single-matrix reverse sweep -------------------------------
+ * The blocked reverse sweep with the columns distributed 1-D block-cyclically
+ * over P ranks: block K = [j, k) of the reverse partition (the short block at the top left,
+ * PAPER.md:704-707) lives on rank K mod P, which stores its column blocks -- ALL n rows of L and
+ * Abar -- side by side in a local n x c_loc column-major array.  Per block, right to left:
+ *   owner:      cd_dist_rev_panel   Cbar <- Cbar D^{-1}; Dbar <- Dbar - tril(Cbar^T C);
+ *                                   Dbar <- chol_unblocked_rev(D, Dbar)
+ *                                   and packs X = [S; Cbar] ((n-j) x w), S = Dbar + Dbar^T
+ *   broadcast X from the owner to every rank (the caller's collective: NCCL / torch.distributed)
+ *   every rank: cd_dist_rev_update  for its column blocks left of the panel (the first q local
+ *                                   columns): Bbar <- Bbar - Cbar R; Rbar <- Rbar - [S; Cbar]^T [R; B]
+ *
+ * The data exchanged per block is X alone; every update is local to the column owner.
+ *
+ * cd_dist_rev_panel: Lk, Ak = the owner's local column block (n rows, w columns, ld ldl / lda >= n),
+ *   global rows; j = the block's first row/column (0-based), 1 <= w <= 128, j + w <= n.
+ *   Ak is updated in place (rows j..n-1); X (device, ld ldx >= n - j) receives [S; Cbar].
+ * cd_dist_rev_update: X from the panel of block [j, j+w); Lq, Aq = the rank's first q local columns
+ *   (all global columns < j); Aq rows j..n-1 are updated in place.  q = 0 is a no-op.
+ * Both: device pointers, asynchronous on `stream`, fp64 / fp32, batch 1, no d_info (check the
+ * diagonal with cd_chol_rev on the owner if needed); ws >= cd_dist_workspace_size(dt, w) bytes.
+ * Returns 0, -i for an invalid i-th argument, or CD_ERR_CUDA. */
+size_t cd_dist_workspace_size(cd_dtype dt, int64_t w);
+int cd_dist_rev_panel(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* Lk, int64_t ldl, void* Ak,
+                      int64_t lda, void* X, int64_t ldx, void* ws, size_t ws_bytes, cd_stream_t stream);
+int cd_dist_rev_update(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* X, int64_t ldx, int64_t q,
+                       const void* Lq, int64_t ldl, void* Aq, int64_t lda, void* ws, size_t ws_bytes,
+                       cd_stream_t stream);
+
 /* Bytes the last cd_chol_host call on this thread moved host -> device and device -> host.
  * fp64 with the fused nb = 128 schedules and TRIL output (the default) pipelines the copies:
  * the lower part of each 128-column block streams in on a library copy stream just before

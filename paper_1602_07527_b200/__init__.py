@@ -86,6 +86,12 @@ def lib():
             L.cd_workspace_size_host.restype = sz
             L.cd_chol_host.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, po, vp, sz, vp]
             L.cd_chol_host.restype = ctypes.c_int
+            L.cd_dist_workspace_size.argtypes = [ctypes.c_int, i64]
+            L.cd_dist_workspace_size.restype = sz
+            L.cd_dist_rev_panel.argtypes = [ctypes.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp]
+            L.cd_dist_rev_panel.restype = ctypes.c_int
+            L.cd_dist_rev_update.argtypes = [ctypes.c_int, i64, i64, i64, vp, i64, i64, vp, i64, vp, i64, vp, sz, vp]
+            L.cd_dist_rev_update.restype = ctypes.c_int
             L.cd_status_string.argtypes = [ctypes.c_int]
             L.cd_status_string.restype = ctypes.c_char_p
             L.cd_last_cuda_error.restype = ctypes.c_char_p

@@ -1489,6 +1489,66 @@ static int sm_count() {
   return cached;
 }
 
+// ------------------------------------------------------------------ distributed reverse steps
+// (include/choldiff.h describes the distribution.)  The same arithmetic as
+// one step of blocked_rev, split at the broadcast: the panel on the column owner, the
+// rank-w updates of the columns left of the panel on every rank.
+template <typename T>
+static void dist_rev_panel(Ctx& c, int n, int j, int w, Opnd Lk, Opnd Ak, Opnd X) {
+  const int k = j + w, p = n - k;
+  T* Dinv = static_cast<T*>(c.take(sizeof(T) * size_t(w) * w));
+  T* part = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
+  run_trinv<T>(c, w, w, true, 1, sub(Lk, j, 0), Dinv);
+  const Opnd Cbar = sub(Ak, k, 0);
+  if (p > 0) {
+    // Cbar <- Cbar D^{-1} (in place: one 128-wide N tile covers the block)
+    Gemm<T>(c, p, w, 0, 0, 1)
+        .seg(Cbar, ws_opnd(Dinv, 0, w), w)
+        .flops(double(p) * w * (w + 1))
+        .run(null_opnd(), Cbar, 1.0, 0.0, 0, part);
+    // Dbar <- Dbar - tril(Cbar^T C)
+    Gemm<T>(c, w, w, 1, 0, 1)
+        .seg(Cbar, sub(Lk, k, 0), p)
+        .flops(double(w) * (w + 1) * p)
+        .run(sub(Ak, j, 0), sub(Ak, j, 0), -1.0, 1.0, 1, part);
+  }
+  // Dbar <- chol_unblocked_rev(D, Dbar), S = Dbar + Dbar^T into the top of X
+  run_sweep_small<T>(c, true, w, 1, sub(Lk, j, 0), sub(Ak, j, 0), 0, X, nullptr);
+  if (p > 0) run_copy<T>(c, p, w, 1, Cbar, sub(X, w, 0));
+}
+
+template <typename T>
+static void dist_rev_update(Ctx& c, int n, int j, int w, Opnd X, int q, Opnd Lq, Opnd Aq) {
+  const int k = j + w, p = n - k;
+  T* part = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
+  if (q <= 0) return;
+  // Bbar <- Bbar - Cbar R
+  if (p > 0)
+    Gemm<T>(c, p, q, 0, 0, 1).seg(sub(X, w, 0), sub(Lq, j, 0), w).run(sub(Aq, k, 0), sub(Aq, k, 0), -1.0, 1.0, 0, part);
+  // Rbar <- Rbar - [S; Cbar]^T [R; B]
+  Gemm<T>(c, w, q, 1, 0, 1).seg(X, sub(Lq, j, 0), n - j).run(sub(Aq, j, 0), sub(Aq, j, 0), -1.0, 1.0, 0, part);
+}
+
+template <typename F>
+static int run_steps(cd_dtype dt, void* ws, size_t ws_bytes, cudaStream_t st, int ws_arg, F&& body) {
+  Ctx pc;
+  pc.plan = true;
+  pc.ws = nullptr;
+  pc.st = nullptr;
+  pc.sms = sm_count();
+  if (dt == CD_F64) body(pc, double(0));
+  else body(pc, float(0));
+  if (pc.off > 0 && (ws == nullptr || ws_bytes < pc.off)) return -ws_arg;
+  Ctx c;
+  c.plan = false;
+  c.ws = static_cast<char*>(ws);
+  c.st = st;
+  c.sms = sm_count();
+  if (dt == CD_F64) body(c, double(0));
+  else body(c, float(0));
+  return c.err;
+}
+
 static size_t plan_size(const Call& k) {
   Ctx c;
   c.plan = true;
@@ -1738,6 +1798,53 @@ int cd_debug_gemm(cd_dtype dt, int64_t M, int64_t N, int64_t K, int ta, int tb, 
   else
     Gemm<float>(c, int(M), int(N), ta, tb, 1).seg(Ao, Bo, int(K)).run(Co, Co, alpha, beta, 0, static_cast<float*>(ws));
   return c.err;
+}
+
+size_t cd_dist_workspace_size(cd_dtype dt, int64_t w) {
+  if ((dt != CD_F64 && dt != CD_F32) || w <= 0) return 0;
+  const size_t es = dt == CD_F64 ? 8 : 4;
+  return (size_t(w) * w * es + 255) / 256 * 256 + size_t(PART_TILES) * G_BM * G_BN * es + 256;
+}
+
+int cd_dist_rev_panel(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* Lk, int64_t ldl, void* Ak,
+                      int64_t lda, void* X, int64_t ldx, void* ws, size_t ws_bytes, cd_stream_t stream) {
+  if (dt != CD_F64 && dt != CD_F32) return -1;
+  if (n < 1 || n > (int64_t(1) << 30)) return -2;
+  if (j < 0 || j >= n) return -3;
+  if (w < 1 || w > DC_NMAX || j + w > n) return -4;
+  if (!Lk) return -5;
+  if (ldl < n) return -6;
+  if (!Ak) return -7;
+  if (lda < n) return -8;
+  if (!X) return -9;
+  if (ldx < n - j) return -10;
+  if (ws_bytes < cd_dist_workspace_size(dt, w)) return -12;
+  const Opnd L{Lk, nullptr, 0, ldl, 0}, A{Ak, nullptr, 0, lda, 0}, Xo{X, nullptr, 0, ldx, 0};
+  return run_steps(dt, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 11, [&](Ctx& c, auto zero) {
+    dist_rev_panel<decltype(zero)>(c, int(n), int(j), int(w), L, A, Xo);
+  });
+}
+
+int cd_dist_rev_update(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* X, int64_t ldx, int64_t q,
+                       const void* Lq, int64_t ldl, void* Aq, int64_t lda, void* ws, size_t ws_bytes,
+                       cd_stream_t stream) {
+  if (dt != CD_F64 && dt != CD_F32) return -1;
+  if (n < 1 || n > (int64_t(1) << 30)) return -2;
+  if (j < 0 || j >= n) return -3;
+  if (w < 1 || w > DC_NMAX || j + w > n) return -4;
+  if (!X) return -5;
+  if (ldx < n - j) return -6;
+  if (q < 0 || q > j) return -7;
+  if (q == 0) return CD_SUCCESS;
+  if (!Lq) return -8;
+  if (ldl < n) return -9;
+  if (!Aq) return -10;
+  if (lda < n) return -11;
+  if (ws_bytes < cd_dist_workspace_size(dt, w)) return -13;
+  const Opnd L{Lq, nullptr, 0, ldl, 0}, A{Aq, nullptr, 0, lda, 0}, Xo{const_cast<void*>(X), nullptr, 0, ldx, 0};
+  return run_steps(dt, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 12, [&](Ctx& c, auto zero) {
+    dist_rev_update<decltype(zero)>(c, int(n), int(j), int(w), Xo, int(q), L, A);
+  });
 }
 
 const char* cd_status_string(int status) {
