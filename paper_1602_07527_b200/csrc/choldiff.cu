@@ -307,10 +307,10 @@ static bool make_tmap_f32_plain(CUtensorMap* map, const void* p, int64_t rows, i
 }
 
 static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
-// TMA epilogue of the tcgen05 GEMM (gemm_tc32.cuh, EPI = 1): on unless CD_TC_EPI=0;
-// CD_TC_EPI_STAGES = operand ring depth with it (2: two CTAs per SM; 3, 4: one)
+// TMA epilogue of the tcgen05 GEMM (gemm_tc32.cuh, EPI = 1, 4-stage ring): on unless CD_TC_EPI=0;
+// 64-wide N tiles for N <= 64 unless CD_TC_BN64=0
 static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
-static int g_tc_epi_stages = getenv("CD_TC_EPI_STAGES") ? atoi(getenv("CD_TC_EPI_STAGES")) : 4;
+static int g_tc_bn64 = getenv("CD_TC_BN64") ? atoi(getenv("CD_TC_BN64")) : 1;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
 
 // ------------------------------------------------------------------ GEMM launcher
@@ -435,6 +435,8 @@ struct Gemm {
     TmaMaps tm;
     memset(&tm, 0, sizeof(tm));
     tm.batched = p.batch > 1 ? 1 : 0;
+    // N tile: 64 for the nb = 64 panels (half the MMA work of a 128-wide tile), else 128
+    const int bn = (p.N <= 64 && g_tc_bn64) ? 64 : 128;
     for (int s = 0; s < p.nseg; ++s) {
       const GemmSeg& sg = p.seg[s];
       if (sg.A.arr || sg.B.arr) return false;
@@ -442,7 +444,7 @@ struct Gemm {
       const T* pb = static_cast<const T*>(sg.B.base) + sg.B.off;
       const bool okA = A_ == 0 ? make_tmap_f32_sw128(&tm.a[s], pa, p.M, sg.K, sg.A.ld, sg.A.stride, p.batch, 32, 32, true)
                                : make_tmap_f32_sw128(&tm.a[s], pa, sg.K, p.M, sg.A.ld, sg.A.stride, p.batch, 32, 128, false);
-      const bool okB = B_ == 0 ? make_tmap_f32_sw128(&tm.b[s], pb, sg.K, p.N, sg.B.ld, sg.B.stride, p.batch, 32, 128, false)
+      const bool okB = B_ == 0 ? make_tmap_f32_sw128(&tm.b[s], pb, sg.K, p.N, sg.B.ld, sg.B.stride, p.batch, 32, bn, false)
                                : make_tmap_f32_sw128(&tm.b[s], pb, p.N, sg.K, sg.B.ld, sg.B.stride, p.batch, 32, 32, true);
       if (!okA || !okB) return false;
     }
@@ -451,11 +453,11 @@ struct Gemm {
     TcEpiMaps em;
     memset(&em, 0, sizeof(em));
     if (tc_epi_maps(em)) {
-      if (g_tc_epi_stages == 4) return launch_tc32_k<A_, B_, 1, 4>(units, tm, em);
-      if (g_tc_epi_stages == 3) return launch_tc32_k<A_, B_, 1, 3>(units, tm, em);
-      return launch_tc32_k<A_, B_, 1, 2>(units, tm, em);
+      if (bn == 64) return launch_tc32_k<A_, B_, 1, 4, 64>(units, tm, em);
+      return launch_tc32_k<A_, B_, 1, 4, 128>(units, tm, em);
     }
-    return launch_tc32_k<A_, B_, 0, TC_STAGES>(units, tm, em);
+    if (bn == 64) return launch_tc32_k<A_, B_, 0, TC_STAGES, 64>(units, tm, em);
+    return launch_tc32_k<A_, B_, 0, TC_STAGES, 128>(units, tm, em);
   }
   // TMA epilogue eligibility (see gemm_tc32.cuh): one split, plain strided D / Cin, 16-byte
   // aligned, and a tril mask only for the in-place update
@@ -474,10 +476,10 @@ struct Gemm {
     }
     return true;
   }
-  template <int A_, int B_, int EPI, int STG>
+  template <int A_, int B_, int EPI, int STG, int BN>
   bool launch_tc32_k(int64_t units, const TmaMaps& tm, const TcEpiMaps& em) {
-    auto kern = k_gemm_tc32<A_, B_, EPI, STG>;
-    constexpr size_t smem = tc_smem(STG, EPI);
+    auto kern = k_gemm_tc32<A_, B_, EPI, STG, BN>;
+    constexpr size_t smem = tc_smem(STG, EPI, BN);
     static int occ = 0;  // per instantiation
     if (!occ) {
       set_smem(kern, smem);

@@ -46,8 +46,8 @@ constexpr uint32_t TC_ECHUNK_BYTES = TC_BM * 32 * 4;              // one 128 x 3
 #endif
 constexpr int TC_ESLOTS = CD_TC_ESLOTS;  // TMA epilogue chunk slots (Cin prefetch depth ESLOTS - 1)
 // stages + (TMA epilogue) chunk slots + barriers / TMEM slot
-__host__ __device__ constexpr size_t tc_smem(int stages, int epi) {
-  return size_t(stages) * TC_STAGE_BYTES + (epi ? TC_ESLOTS * TC_ECHUNK_BYTES : 0) + 1024 + 256;
+__host__ __device__ constexpr size_t tc_smem(int stages, int epi, int bn = TC_BN) {
+  return size_t(stages) * (TC_BM + bn) * TC_BK * 4 + (epi ? TC_ESLOTS * TC_ECHUNK_BYTES : 0) + 1024 + 256;
 }
 constexpr size_t TC_SMEM = tc_smem(TC_STAGES, 0);
 
@@ -83,12 +83,12 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // instruction descriptor: D f32, A/B tf32, M=128, N=128, majors per operand
-__host__ __device__ constexpr uint32_t tc_idesc(int a_mn_major, int b_mn_major) {
+__host__ __device__ constexpr uint32_t tc_idesc(int a_mn_major, int b_mn_major, int n = 128) {
   return (1u << 4)                       // c_format = F32
          | (2u << 7) | (2u << 10)        // a_format = b_format = TF32
          | (uint32_t(a_mn_major) << 15)  // a_major (1 = MN)
          | (uint32_t(b_mn_major) << 16)  // b_major
-         | ((128u >> 3) << 17)           // N >> 3
+         | ((uint32_t(n) >> 3) << 17)    // N >> 3
          | ((128u >> 4) << 24);          // M >> 4
 }
 
@@ -144,16 +144,19 @@ __host__ __device__ constexpr int tcp_threads(int epi) { return (tc_conv_warp0(e
 //          ~1.7 TB/s).  Host-side conditions: splits == 1,
 //          D (and Cin) TMA-describable, and a tril mask only for the in-place update
 //          (masked elements are written back unchanged).
-// STG = depth of the operand ring.
-template <int TA, int TB, int EPI, int STG>
+// STG = depth of the operand ring.  BN = the N tile (128, or 64 for the nb = 64 panels: M x 64
+// products would otherwise issue half-empty MMAs -- the batched forward update is tensor-bound).
+template <int TA, int TB, int EPI, int STG, int BN>
 __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
     k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm, const __grid_constant__ TcEpiMaps em) {
   constexpr int TC_STAGES = STG;
+  constexpr int TC_BN = BN;
+  constexpr uint32_t TC_STAGE_BYTES = (TC_BM + BN) * TC_BK * 4;
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_tc) + 1023) & ~uintptr_t(1023));
   unsigned char* As = base;                                   // stages of A (16 KB each)
-  unsigned char* Bs = base + TC_STAGES * (TC_BM * TC_BK * 4);  // stages of B (16 KB each)
+  unsigned char* Bs = base + TC_STAGES * (TC_BM * TC_BK * 4);  // stages of B (BN x 32 fp32 each)
   unsigned char* Es = base + TC_STAGES * TC_STAGE_BYTES;      // EPI: 128 x 32 chunk slots
   uint64_t* full = reinterpret_cast<uint64_t*>(Es + (EPI ? TC_ESLOTS * TC_ECHUNK_BYTES : 0));
   uint64_t* empty = full + TC_STAGES;
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
             else tma_load_2d(as, &tm.a[sg], kl, m0, &full[s]);
           }
           if (TB == 1) {  // MN-major B
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < BN / 32; ++c) {
               if (tm.batched) tma_load_3d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, int(b), &full[s]);
               else tma_load_2d(bs + c * 4096, &tm.b[sg], n0 + 32 * c, kl, &full[s]);
             }
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = tc_idesc(TA == 0 ? 1 : 0, TB == 1 ? 1 : 0);
+      constexpr uint32_t idesc = tc_idesc(TA == 0 ? 1 : 0, TB == 1 ? 1 : 0, BN);
       int it = 0, i = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
         int m0, n0, split, kt0, nkt;
@@ -308,11 +311,11 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
         float4* b4 = reinterpret_cast<float4*>(Bs + s * (TC_BN * TC_BK * 4));
 #pragma unroll 4
         for (int e = ct; e < TC_BM * TC_BK / 4; e += TC_CONVW * 32) {
-          float4 x = a4[e], y = b4[e];
+          float4 x = a4[e];
+          float4 y = e < BN * TC_BK / 4 ? b4[e] : float4{};
           x = tf32_rna4(x);
-          y = tf32_rna4(y);
           a4[e] = x;
-          b4[e] = y;
+          if (e < BN * TC_BK / 4) b4[e] = tf32_rna4(y);
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();

@@ -33,7 +33,8 @@ def colmajor(r, c, dtype):
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (200, 136, 72), (64, 300, 1000), (257, 129, 40)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (200, 136, 72), (64, 300, 1000), (257, 129, 40), (300, 64, 200),
+                                   (129, 40, 96), (512, 33, 64)])
 def test_gemm_layouts(dtype, ta, tb, M, N, K):
     torch.manual_seed(M * 7 + N + K)
     A = colmajor(K, M, dtype) if ta else colmajor(M, K, dtype)
