@@ -162,7 +162,7 @@ int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t l
                                       const cd_opts* opts, void* ws, size_t ws_bytes, int* d_info,
                                       cd_stream_t stream);
 
-/* ---- Distributed single-matrix reverse sweep -------------------------------
+/* ---- Distributed single-matrix sweeps -------------------------------------
  * The blocked reverse sweep with the columns distributed 1-D block-cyclically
  * over P ranks: block K = [j, k) of the reverse partition (the short block at the top left,
  * PAPER.md:704-707) lives on rank K mod P, which stores its column blocks -- ALL n rows of L and
@@ -190,6 +190,24 @@ int cd_dist_rev_panel(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* 
 int cd_dist_rev_update(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* X, int64_t ldx, int64_t q,
                        const void* Lq, int64_t ldl, void* Aq, int64_t lda, void* ws, size_t ws_bytes,
                        cd_stream_t stream);
+
+/* Distributed forward sweep, same distribution and block partition as above
+ * (any partition is exact), blocks left to right.  Per block [j, k):
+ *   every rank: cd_dist_fwd_partial  Z_r = [Adot L][j:n, its first q local columns] .
+ *                                         [L Adot][j:k, same columns]^T     ((n-j) x w, ldz = n - j;
+ *                                         zero when q = 0) -- its share of [Rdot R^T + R Rdot^T ;
+ *                                         Bdot R^T + B Rdot^T]
+ *   sum-reduce Z_r onto the owner (the caller's collective)
+ *   owner:      cd_dist_fwd_panel    Ddot <- Ddot - tril(Z_top); Cdot <- Cdot - Z_bottom;
+ *                                    Ddot <- chol_unblocked_fwd(D, Ddot); Cdot <- (Cdot - C Ddot^T) D^{-T}
+ *
+ * Adot holds tril(Sigma_dot) in and L_dot out (the owner's block rows j..n-1).  Arguments and
+ * errors as for the reverse steps. */
+int cd_dist_fwd_partial(cd_dtype dt, int64_t n, int64_t j, int64_t w, int64_t q, const void* Lq, int64_t ldl,
+                        const void* Aq, int64_t lda, void* Z, int64_t ldz, void* ws, size_t ws_bytes,
+                        cd_stream_t stream);
+int cd_dist_fwd_panel(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* Lk, int64_t ldl, void* Ak,
+                      int64_t lda, const void* Z, int64_t ldz, void* ws, size_t ws_bytes, cd_stream_t stream);
 
 /* Bytes the last cd_chol_host call on this thread moved host -> device and device -> host.
  * fp64 with the fused nb = 128 schedules and TRIL output (the default) pipelines the copies:

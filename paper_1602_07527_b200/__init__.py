@@ -92,6 +92,10 @@ def lib():
             L.cd_dist_rev_panel.restype = ctypes.c_int
             L.cd_dist_rev_update.argtypes = [ctypes.c_int, i64, i64, i64, vp, i64, i64, vp, i64, vp, i64, vp, sz, vp]
             L.cd_dist_rev_update.restype = ctypes.c_int
+            L.cd_dist_fwd_partial.argtypes = [ctypes.c_int, i64, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp]
+            L.cd_dist_fwd_partial.restype = ctypes.c_int
+            L.cd_dist_fwd_panel.argtypes = [ctypes.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp]
+            L.cd_dist_fwd_panel.restype = ctypes.c_int
             L.cd_status_string.argtypes = [ctypes.c_int]
             L.cd_status_string.restype = ctypes.c_char_p
             L.cd_last_cuda_error.restype = ctypes.c_char_p

@@ -1531,6 +1531,55 @@ static void dist_rev_update(Ctx& c, int n, int j, int w, Opnd X, int q, Opnd Lq,
   Gemm<T>(c, w, q, 1, 0, 1).seg(X, sub(Lq, j, 0), n - j).run(sub(Aq, j, 0), sub(Aq, j, 0), -1.0, 1.0, 0, part);
 }
 
+// Forward, block [j, k) on its owner; Z = the sum over all ranks of
+// [Adot[j:n, cols] L[j:n, cols]] [L[j:k, cols] Adot[j:k, cols]]^T for their columns left of the
+// block, i.e. [Rdot R^T + R Rdot^T ; Bdot R^T + B Rdot^T].
+template <typename T>
+static void dist_fwd_partial(Ctx& c, int n, int j, int w, int q, Opnd Lq, Opnd Aq, Opnd Z) {
+  T* part = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
+  if (c.plan || !c.ok()) return;
+  if (q == 0) {  // no columns left of the block on this rank: a zero contribution
+    c.err = note_cuda(cudaMemsetAsync(const_cast<void*>(Z.base), 0, sizeof(T) * size_t(n - j) * w, c.st));  // ldz = n - j
+    return;
+  }
+  Gemm<T>(c, n - j, w, 0, 1, 1)
+      .seg(sub(Aq, j, 0), sub(Lq, j, 0), q)
+      .seg(sub(Lq, j, 0), sub(Aq, j, 0), q)
+      .run(null_opnd(), Z, 1.0, 0.0, 0, part);
+}
+
+template <typename T>
+static void dist_fwd_panel(Ctx& c, int n, int j, int w, Opnd Lk, Opnd Ak, Opnd Z) {
+  const int k = j + w, p = n - k;
+  T* Dinv = static_cast<T*>(c.take(sizeof(T) * size_t(w) * w));
+  T* Dcw = static_cast<T*>(c.take(sizeof(T) * size_t(w) * w));
+  T* part = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
+  run_trinv<T>(c, w, w, false, 1, sub(Lk, j, 0), Dinv);
+  if (!c.plan && c.ok()) {
+    // Ddot <- Ddot - tril(Rdot R^T + R Rdot^T);  Cdot <- Cdot - Bdot R^T - B Rdot^T
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_sub<T><<<grid_1d(int64_t(w) * w, 256, c.sms), 256, 0, c.st>>>(w, w, Z, sub(Ak, j, 0), 1);
+    c.launched();
+    if (p > 0) {
+      c.pre(CD_PROF_OTHER, 0.0);
+      k_sub<T><<<grid_1d(int64_t(p) * w, 256, c.sms), 256, 0, c.st>>>(p, w, sub(Z, w, 0), sub(Ak, k, 0), 0);
+      c.launched();
+    }
+  }
+  const Opnd Dc = ws_opnd(Dcw, 0, w);
+  // Ddot <- chol_unblocked_fwd(D, Ddot) (+ the clean copy Dc = tril(Ddot))
+  run_sweep_small<T>(c, false, w, 1, sub(Lk, j, 0), sub(Ak, j, 0), 0, p > 0 ? Dc : null_opnd(), nullptr);
+  if (p > 0) {
+    // Cdot <- (Cdot - C Ddot^T) D^{-T}
+    const Opnd Cd = sub(Ak, k, 0);
+    Gemm<T>(c, p, w, 0, 1, 1).seg(sub(Lk, k, 0), Dc, w).run(Cd, Cd, -1.0, 1.0, 0, part);
+    Gemm<T>(c, p, w, 0, 1, 1)
+        .seg(Cd, ws_opnd(Dinv, 0, w), w)
+        .flops(double(p) * w * (w + 1))
+        .run(null_opnd(), Cd, 1.0, 0.0, 0, part);
+  }
+}
+
 template <typename F>
 static int run_steps(cd_dtype dt, void* ws, size_t ws_bytes, cudaStream_t st, int ws_arg, F&& body) {
   Ctx pc;
@@ -1805,7 +1854,7 @@ int cd_debug_gemm(cd_dtype dt, int64_t M, int64_t N, int64_t K, int ta, int tb, 
 size_t cd_dist_workspace_size(cd_dtype dt, int64_t w) {
   if ((dt != CD_F64 && dt != CD_F32) || w <= 0) return 0;
   const size_t es = dt == CD_F64 ? 8 : 4;
-  return (size_t(w) * w * es + 255) / 256 * 256 + size_t(PART_TILES) * G_BM * G_BN * es + 256;
+  return 2 * ((size_t(w) * w * es + 255) / 256 * 256) + size_t(PART_TILES) * G_BM * G_BN * es + 256;
 }
 
 int cd_dist_rev_panel(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* Lk, int64_t ldl, void* Ak,
@@ -1846,6 +1895,46 @@ int cd_dist_rev_update(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void*
   const Opnd L{Lq, nullptr, 0, ldl, 0}, A{Aq, nullptr, 0, lda, 0}, Xo{const_cast<void*>(X), nullptr, 0, ldx, 0};
   return run_steps(dt, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 12, [&](Ctx& c, auto zero) {
     dist_rev_update<decltype(zero)>(c, int(n), int(j), int(w), Xo, int(q), L, A);
+  });
+}
+
+int cd_dist_fwd_partial(cd_dtype dt, int64_t n, int64_t j, int64_t w, int64_t q, const void* Lq, int64_t ldl,
+                        const void* Aq, int64_t lda, void* Z, int64_t ldz, void* ws, size_t ws_bytes,
+                        cd_stream_t stream) {
+  if (dt != CD_F64 && dt != CD_F32) return -1;
+  if (n < 1 || n > (int64_t(1) << 30)) return -2;
+  if (j < 0 || j >= n) return -3;
+  if (w < 1 || w > DC_NMAX || j + w > n) return -4;
+  if (q < 0 || q > j) return -5;
+  if (q > 0 && !Lq) return -6;
+  if (q > 0 && ldl < n) return -7;
+  if (q > 0 && !Aq) return -8;
+  if (q > 0 && lda < n) return -9;
+  if (!Z) return -10;
+  if (ldz != n - j) return -11;
+  if (ws_bytes < cd_dist_workspace_size(dt, w)) return -13;
+  const Opnd L{Lq, nullptr, 0, ldl, 0}, A{Aq, nullptr, 0, lda, 0}, Zo{Z, nullptr, 0, ldz, 0};
+  return run_steps(dt, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 12, [&](Ctx& c, auto zero) {
+    dist_fwd_partial<decltype(zero)>(c, int(n), int(j), int(w), int(q), L, A, Zo);
+  });
+}
+
+int cd_dist_fwd_panel(cd_dtype dt, int64_t n, int64_t j, int64_t w, const void* Lk, int64_t ldl, void* Ak,
+                      int64_t lda, const void* Z, int64_t ldz, void* ws, size_t ws_bytes, cd_stream_t stream) {
+  if (dt != CD_F64 && dt != CD_F32) return -1;
+  if (n < 1 || n > (int64_t(1) << 30)) return -2;
+  if (j < 0 || j >= n) return -3;
+  if (w < 1 || w > DC_NMAX || j + w > n) return -4;
+  if (!Lk) return -5;
+  if (ldl < n) return -6;
+  if (!Ak) return -7;
+  if (lda < n) return -8;
+  if (!Z) return -9;
+  if (ldz < n - j) return -10;
+  if (ws_bytes < cd_dist_workspace_size(dt, w)) return -12;
+  const Opnd L{Lk, nullptr, 0, ldl, 0}, A{Ak, nullptr, 0, lda, 0}, Zo{Z, nullptr, 0, ldz, 0};
+  return run_steps(dt, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 11, [&](Ctx& c, auto zero) {
+    dist_fwd_panel<decltype(zero)>(c, int(n), int(j), int(w), L, A, Zo);
   });
 }
 

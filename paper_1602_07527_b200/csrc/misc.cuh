@@ -35,6 +35,19 @@ __global__ void k_copy(int M, int N, int64_t batch, Opnd S, Opnd D) {
   }
 }
 
+// D(r, c) -= S(r, c) over an M x N view (tril: only r >= c), one matrix -- the distributed
+// forward sweep's application of the reduced partial products (include/choldiff.h).
+template <typename T>
+__global__ void k_sub(int M, int N, Opnd S, Opnd D, int tril) {
+  const int64_t total = int64_t(M) * N;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(idx % M), c = int(idx / M);
+    if (tril && r < c) continue;
+    optr_w<T>(D, 0)[r + int64_t(c) * D.ld] -= optr<T>(S, 0)[r + int64_t(c) * S.ld];
+  }
+}
+
 // D(i, j) = S(i, j) for i >= j (lower triangles only), n x n per batch entry.
 template <typename T>
 __global__ void k_copy_tril(int n, int64_t batch, Opnd S, Opnd D) {

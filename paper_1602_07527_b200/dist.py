@@ -13,6 +13,14 @@ ld = n.  Per block, right to left:
     all:    update  Bbar <- Bbar - Cbar R;  Rbar <- Rbar - X^T [R; B]  on the rank's columns left
                     of the panel (a prefix of its storage: its blocks are stored in order)
 
+Forward mode on the same distribution and partition, blocks left to right:
+
+    all:    partial Z_r = [Adot L][j:n, cols] [L Adot][j:k, cols]^T over the rank's columns left of
+                    the block (its share of [Rdot R^T + R Rdot^T ; Bdot R^T + B Rdot^T])
+    all:    sum-reduce of Z onto the owner (the one exchange per block)
+    owner:  panel   Ddot -= tril(Z_top); Cdot -= Z_bottom; Ddot <- chol_unblocked_fwd(D, Ddot);
+                    Cdot <- (Cdot - C Ddot^T) D^-T
+
 Every arithmetic step runs in libcholdiff's kernels (CudaSteps); this module is the host loop and the
 ownership bookkeeping.  `bcast(tensor, src_rank)` is torch.distributed.broadcast for a process group
 (chol_rev_distributed) or a no-op when all ranks live in one process (chol_rev_loopback, which runs
@@ -90,6 +98,16 @@ class CudaSteps:
         _check(self.L.cd_dist_rev_update(self.dt, n, j, w, X.data_ptr(), n - j, q, Lq.data_ptr(), n,
                                          Aq.data_ptr(), n, self.ws.data_ptr(), self.ws_bytes, self._stream()))
 
+    def fwd_partial(self, n, j, w, q, Lq, Aq, Z):
+        lp = Lq.data_ptr() if q else None
+        ap = Aq.data_ptr() if q else None
+        _check(self.L.cd_dist_fwd_partial(self.dt, n, j, w, q, lp, n, ap, n, Z.data_ptr(), n - j,
+                                          self.ws.data_ptr(), self.ws_bytes, self._stream()))
+
+    def fwd_panel(self, n, j, w, Lk, Ak, Z):
+        _check(self.L.cd_dist_fwd_panel(self.dt, n, j, w, Lk.data_ptr(), n, Ak.data_ptr(), n, Z.data_ptr(), n - j,
+                                        self.ws.data_ptr(), self.ws_bytes, self._stream()))
+
 
 def run_schedule(n: int, nb: int, rank: int, world: int, Lloc: torch.Tensor, Aloc: torch.Tensor, steps, bcast,
                  xbuf: torch.Tensor | None = None) -> torch.Tensor:
@@ -108,6 +126,70 @@ def run_schedule(n: int, nb: int, rank: int, world: int, Lloc: torch.Tensor, Alo
         q = sum(ww for (KK, (_, ww, _)) in mine.items() if KK < K)
         steps.update(n, j, w, Xk, q, Lloc[:q], Aloc[:q])
     return Aloc
+
+
+def run_schedule_fwd(n: int, nb: int, rank: int, world: int, Lloc: torch.Tensor, Aloc: torch.Tensor, steps,
+                     reduce, zbuf: torch.Tensor | None = None) -> torch.Tensor:
+    """Forward host loop of one rank: Aloc (storage of tril(Sigma_dot) columns) -> L_dot columns, in place.
+    `reduce(tensor, dst_rank)` sums the ranks' tensors onto dst."""
+    mine = {K: (j, w, co) for (K, j, w, co) in owned_blocks(n, nb, rank, world)}
+    Z = zbuf if zbuf is not None else Aloc.new_empty(n * nb)
+    for K, (j, w) in enumerate(reverse_blocks(n, nb)):
+        Zk = Z[: (n - j) * w]
+        q = sum(ww for (KK, (_, ww, _)) in mine.items() if KK < K)
+        steps.fwd_partial(n, j, w, q, Lloc[:q], Aloc[:q], Zk)
+        owner = K % world
+        reduce(Zk, owner)
+        if owner == rank:
+            _, _, co = mine[K]
+            steps.fwd_panel(n, j, w, Lloc[co:co + w], Aloc[co:co + w], Zk)
+    return Aloc
+
+
+def chol_fwd_distributed(Lloc: torch.Tensor, Aloc: torch.Tensor, n: int, nb: int = 128, group=None,
+                         steps=None) -> torch.Tensor:
+    """One rank of the distributed forward sweep (Aloc: storage of tril(Sigma_dot) -> L_dot)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if Lloc.shape != Aloc.shape or Lloc.dtype != Aloc.dtype:
+        raise ValueError("Lloc and Aloc must be storage tensors of the same shape and dtype")
+    if steps is None:
+        if not Aloc.is_cuda:
+            raise CholdiffError("chol_fwd_distributed runs on CUDA storage tensors (no CPU fallback)")
+        steps = CudaSteps(Aloc.device, Aloc.dtype, nb)
+    ranks = None if group is None else dist.get_process_group_ranks(group)
+
+    def reduce(t, dst):
+        dist.reduce(t, dst if ranks is None else ranks[dst], op=dist.ReduceOp.SUM, group=group)
+
+    return run_schedule_fwd(n, nb, rank, world, Lloc, Aloc, steps, reduce)
+
+
+def chol_fwd_loopback(L: torch.Tensor, Sdot: torch.Tensor, nb: int, world: int, steps=None) -> torch.Tensor:
+    """The distributed forward schedule for `world` simulated ranks in this process: each rank's partial
+    is computed into its own buffer and summed in place of the reduction; returns L_dot (n, n)."""
+    n = L.shape[-1]
+    Ls = [local_columns(L, nb, r, world) for r in range(world)]
+    As = [local_columns(Sdot, nb, r, world) for r in range(world)]
+    if steps is None:
+        if not L.is_cuda:
+            raise CholdiffError("chol_fwd_loopback runs on CUDA tensors (no CPU fallback)")
+        steps = CudaSteps(L.device, L.dtype, nb)
+    mine = [{K: (j, w, co) for (K, j, w, co) in owned_blocks(n, nb, r, world)} for r in range(world)]
+    Zs = [L.new_empty(n * nb) for _ in range(world)]
+    for K, (j, w) in enumerate(reverse_blocks(n, nb)):
+        m = (n - j) * w
+        for r in range(world):
+            q = sum(ww for (KK, (_, ww, _)) in mine[r].items() if KK < K)
+            steps.fwd_partial(n, j, w, q, Ls[r][:q], As[r][:q], Zs[r][:m])
+        o = K % world
+        for r in range(world):
+            if r != o:
+                Zs[o][:m] += Zs[r][:m]  # the reduction (a device add; the arithmetic of the method stays in the steps)
+        _, _, co = mine[o][K]
+        steps.fwd_panel(n, j, w, Ls[o][co:co + w], As[o][co:co + w], Zs[o][:m])
+    return assemble(As, n, nb)
 
 
 def chol_rev_distributed(Lloc: torch.Tensor, Aloc: torch.Tensor, n: int, nb: int = 128, group=None,

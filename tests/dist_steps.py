@@ -31,3 +31,26 @@ class NumpySteps:
         Xm = X.numpy().reshape(w, n - j).T
         Am[k:n, :] -= Xm[w:, :] @ Lm[j:k, :]  # Bbar <- Bbar - Cbar R
         Am[j:k, :] -= Xm.T @ Lm[j:n, :]  # Rbar <- Rbar - [S; Cbar]^T [R; B]
+
+    def fwd_partial(self, n, j, w, q, Lq, Aq, Z):
+        Zm = Z.numpy().reshape(w, n - j).T
+        if q == 0:
+            Zm[:] = 0.0
+            return
+        k = j + w
+        Lm = Lq.numpy().T
+        Am = Aq.numpy().T
+        Zm[:] = Am[j:n, :] @ Lm[j:k, :].T + Lm[j:n, :] @ Am[j:k, :].T
+
+    def fwd_panel(self, n, j, w, Lk, Ak, Z):
+        k = j + w
+        Lm = Lk.numpy().T
+        Am = Ak.numpy().T
+        Zm = Z.numpy().reshape(w, n - j).T
+        D = np.tril(Lm[j:k, :])
+        Dd = np.tril(Am[j:k, :]) - np.tril(Zm[:w, :])
+        Dd = np.tril(oracle.chol_fwd(D, Dd + np.tril(Dd, -1).T))  # chol_unblocked_fwd on the block
+        Am[j:k, :] = Dd
+        if k < n:
+            Cd = Am[k:n, :] - Zm[w:, :]
+            Am[k:n, :] = (Cd - Lm[k:n, :] @ Dd.T) @ np.linalg.inv(D).T

@@ -43,6 +43,15 @@ def test_loopback_schedule_matches_oracle(n, nb, world):
     assert _rel(out.numpy(), oracle.chol_rev(L, Lb)) < 1e-12
 
 
+@pytest.mark.parametrize("n,nb,world", [(40, 8, 1), (40, 8, 2), (37, 8, 3), (50, 16, 4)])
+def test_loopback_fwd_schedule_matches_oracle(n, nb, world):
+    L, _, Sd = synthetic.draw(n, 950 + n, lbar=False, sdot=True)
+    S_poison = np.tril(Sd) + np.triu(np.full((n, n), np.nan), 1)
+    out = cdd.chol_fwd_loopback(torch.from_numpy(L), torch.from_numpy(S_poison), nb, world, steps=NumpySteps())
+    ref = oracle.chol_fwd(L, Sd)
+    assert _rel(out.numpy(), ref) < 1e-12
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -60,8 +69,13 @@ def _worker(rank, world, port, n, nb, q):
         cdd.chol_rev_distributed(Lloc, Aloc, n, nb, steps=NumpySteps())
         gathered = [None] * world
         dist.all_gather_object(gathered, Aloc)
+        _, _, Sd = synthetic.draw(n, 78, lbar=False, sdot=True)
+        Sloc = cdd.local_columns(torch.from_numpy(np.tril(Sd)), nb, rank, world)
+        cdd.chol_fwd_distributed(Lloc, Sloc, n, nb, steps=NumpySteps())
+        gathered_f = [None] * world
+        dist.all_gather_object(gathered_f, Sloc)
         if rank == 0:
-            q.put(cdd.assemble(gathered, n, nb).numpy())
+            q.put((cdd.assemble(gathered, n, nb).numpy(), cdd.assemble(gathered_f, n, nb).numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -75,12 +89,14 @@ def test_two_rank_gloo_matches_oracle(n, nb):
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, nb, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = q.get(timeout=120)
+    out, outf = q.get(timeout=120)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     L, Lb, _ = synthetic.draw(n, 77)
     assert _rel(out, oracle.chol_rev(L, Lb)) < 1e-12
+    _, _, Sd = synthetic.draw(n, 78, lbar=False, sdot=True)
+    assert _rel(outf, oracle.chol_fwd(L, Sd)) < 1e-12
 
 
 @pytest.mark.gpu
@@ -101,6 +117,22 @@ def test_gpu_loopback_matches_oracle(n, nb, world, dt):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n,nb,world,dt", [(300, 128, 2, torch.float64), (1000, 64, 3, torch.float64),
+                                           (1000, 128, 4, torch.float64), (513, 128, 2, torch.float32),
+                                           (256, 128, 1, torch.float64), (40, 16, 2, torch.float64)])
+def test_gpu_fwd_loopback_matches_oracle(n, nb, world, dt):
+    from gpu_helpers import fp32_round
+    L, _, Sd = synthetic.draw(n, 1700 + n, lbar=False, sdot=True)
+    if dt == torch.float32:
+        L, Sd = fp32_round(L, Sd)
+    S_poison = np.tril(Sd) + np.triu(np.full((n, n), np.nan), 1)
+    out = cdd.chol_fwd_loopback(torch.from_numpy(L).to(dt).cuda(), torch.from_numpy(S_poison).to(dt).cuda(), nb,
+                                world)
+    torch.cuda.synchronize()
+    assert _rel(out.double().cpu().numpy(), oracle.chol_fwd(L, Sd)) < (1e-10 if dt == torch.float64 else 1e-4)
+
+
+@pytest.mark.gpu
 def test_gpu_nccl_single_rank_group():
     # the torch.distributed path itself (NCCL broadcasts of X) on a one-rank group
     n, nb = 700, 128
@@ -112,7 +144,12 @@ def test_gpu_nccl_single_rank_group():
         Aloc = cdd.local_columns(torch.from_numpy(Lb).cuda(), nb, 0, 1)
         cdd.chol_rev_distributed(Lloc, Aloc, n, nb)
         out = cdd.assemble([Aloc], n, nb)
+        _, _, Sd = synthetic.draw(n, 4243, lbar=False, sdot=True)
+        Sloc = cdd.local_columns(torch.from_numpy(np.tril(Sd)).cuda(), nb, 0, 1)
+        cdd.chol_fwd_distributed(Lloc, Sloc, n, nb)
+        outf = cdd.assemble([Sloc], n, nb)
         torch.cuda.synchronize()
     finally:
         dist.destroy_process_group()
     assert _rel(out.cpu().numpy(), oracle.chol_rev(L, Lb)) < 1e-10
+    assert _rel(outf.cpu().numpy(), oracle.chol_fwd(L, Sd)) < 1e-10
