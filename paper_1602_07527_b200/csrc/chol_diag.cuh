@@ -148,10 +148,8 @@ __global__ void __launch_bounds__(DC_THREADS, 1)
   }
   __syncthreads();
   TIO* X = Dinv + b * stride_i;
-  for (int e = tid; e < w * w; e += DC_THREADS) {
-    const int i = e % w, c = e / w;
-    X[i + int64_t(c) * ldi] = TIO((i >= c) ? sX[tat(NBLK, i, c)] : 0.0);
-  }
+  for (int c = warp; c < w; c += DC_WARPS)
+    for (int i = lane; i < w; i += 32) X[i + int64_t(c) * ldi] = TIO((i >= c) ? sX[tat(NBLK, i, c)] : 0.0);
 }
 
 }  // namespace cd
