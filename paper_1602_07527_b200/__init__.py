@@ -236,6 +236,31 @@ def chol_fwd(L: torch.Tensor, Sdot: torch.Tensor, *, nb=None, route: str = "auto
     return _run(CD_OP_FWD, L, A, nb, route, "tril", info)
 
 
+_side_streams: dict = {}
+
+
+def chol_rev_fwd(L: torch.Tensor, Lbar: torch.Tensor, Sdot: torch.Tensor, *, nb=None, inplace: bool = True):
+    """Both sensitivities of one factor (configs[3]'s workload): Sigma_bar = chol_rev(L, Lbar) on the
+    current stream and L_dot = chol_fwd(L, Sdot) on a side stream, joined back into the current
+    stream before returning.  The two sweeps are independent, so their latency-bound diagonal-block
+    launches fill the gaps of each other's bandwidth-bound updates.  Returns (Sigma_bar, L_dot)."""
+    dev = Lbar.device
+    cur = torch.cuda.current_stream(dev)
+    side = _side_streams.get(dev.index)
+    if side is None:
+        side = _side_streams[dev.index] = torch.cuda.Stream(dev)
+    Lc, A = _prep(L, Lbar, inplace)
+    _, F = _prep(Lc, Sdot, inplace)
+    side.wait_stream(cur)
+    r = _run(CD_OP_REV, Lc, A, nb, "auto", "tril", False)
+    with torch.cuda.stream(side):
+        f = _run(CD_OP_FWD, Lc, F, nb, "auto", "tril", False)
+    cur.wait_stream(side)
+    for t in (Lc, F):
+        t.record_stream(side)
+    return r, f
+
+
 def chol_fwd_fused(Sigma: torch.Tensor, Sdot: torch.Tensor, *, info: bool = False):
     """Fused factorisation + forward mode (cd_chol_fwd_fused, fp64): in place, tril(Sigma) ->
     L with Sigma = L L^T and tril(Sdot) -> L_dot, in one sweep.

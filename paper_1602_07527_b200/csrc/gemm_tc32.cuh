@@ -228,11 +228,14 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
           if (p.nseg > 1 && kt * TC_BK >= p.seg[1].kv0) sg = 1;
           if (p.nseg > 2 && kt * TC_BK >= p.seg[2].kv0) sg = 2;
           const int kl = kt * TC_BK - p.seg[sg].kv0;
-          mbar_expect_tx(&full[s], TC_STAGE_BYTES);
+          // MN-major A: boxes wholly below row M are not loaded (their accumulator rows are
+          // never stored), so short panels (M = 64) move no zero fill
+          const int na = TA == 0 ? min(4, (p.M - m0 + 31) / 32) : 4;
+          mbar_expect_tx(&full[s], TC_STAGE_BYTES - uint32_t(4 - na) * 4096u);
           unsigned char* as = As + s * (TC_BM * TC_BK * 4);
           unsigned char* bs = Bs + s * (TC_BN * TC_BK * 4);
           if (TA == 0) {  // MN-major: four 32(M) x 32(K) boxes
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < na; ++c) {
               if (tm.batched) tma_load_3d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, int(b), &full[s]);
               else tma_load_2d(as + c * 4096, &tm.a[sg], m0 + 32 * c, kl, &full[s]);
             }
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
         tc_wait(&full[s], (it / TC_STAGES) & 1);
         float4* a4 = reinterpret_cast<float4*>(As + s * (TC_BM * TC_BK * 4));
         float4* b4 = reinterpret_cast<float4*>(Bs + s * (TC_BN * TC_BK * 4));
+#ifndef CD_TC_NOROUND  // (measurement switch: the stage handshake without the rounding pass)
 #pragma unroll 4
         for (int e = ct; e < TC_BM * TC_BK / 4; e += TC_CONVW * 32) {
           float4 x = a4[e];
@@ -317,6 +321,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
           a4[e] = x;
           if (e < BN * TC_BK / 4) b4[e] = tf32_rna4(y);
         }
+#endif
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[s]);

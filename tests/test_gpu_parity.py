@@ -267,6 +267,17 @@ def test_f32_blocked_sizes(n, B):
     assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL32
 
 
+@pytest.mark.parametrize("n,B,dt", [(300, 3, torch.float64), (512, 2, torch.float32), (40, 5, torch.float64)])
+def test_rev_fwd_two_streams_equal_separate_calls(n, B, dt):
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=8 * n, sdot=True)
+    Lt, Lbt, St = to_dev(L, dt), to_dev(Lb, dt), to_dev(np.tril(Sd), dt)
+    r1 = cd.chol_rev(Lt, Lbt.clone())
+    f1 = cd.chol_fwd(Lt, St.clone())
+    r2, f2 = cd.chol_rev_fwd(Lt, Lbt.clone(), St.clone())
+    torch.cuda.synchronize()
+    assert torch.equal(torch.tril(r1), torch.tril(r2)) and torch.equal(torch.tril(f1), torch.tril(f2))
+
+
 @pytest.mark.parametrize("nb", [64, 128])
 def test_f32_tf32_rounded_operands(nb):
     # the tcgen05 GEMM rounds its operands to tf32 (cvt.rna) instead of letting the
