@@ -562,7 +562,8 @@ def bench_small_configs(args, dist: Dist):
     t = dist.max(statistics.median(timed_steps(step, restore, 5, args.warmup, dist, stream)))
     fl = (rev_flops(n) + fwd_flops(n)) * total
     out["batched_f32_n512"] = {
-        "workload": f"configs[3]: fp32 rev + fwd, {total} x N={n}, sharded by matrix over {P} GPU(s)",
+        "workload": f"configs[3]: fp32 rev + fwd, {total} x N={n}, sharded by matrix over {P} GPU(s); "
+                    "cd.chol_rev_fwd (the two independent sweeps on two streams)",
         "ms_per_step": round(t, 3), "matrices_per_s": round(total / (t * 1e-3), 1),
         "gflops": round(fl / (t * 1e-3) / 1e9, 1),
         # engines: tcgen05 kind::tf32 GEMMs + fp64-DMMA on-chip diagonal blocks.  Roofline =
