@@ -309,6 +309,9 @@ static bool make_tmap_f32_plain(CUtensorMap* map, const void* p, int64_t rows, i
 static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
 // TMA epilogue of the tcgen05 GEMM (gemm_tc32.cuh, EPI = 1, 4-stage ring): on unless CD_TC_EPI=0;
 // 64-wide N tiles for N <= 64 unless CD_TC_BN64=0
+#ifndef CD_TC_EPI_STG
+#define CD_TC_EPI_STG 4
+#endif
 static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
 static int g_tc_bn64 = getenv("CD_TC_BN64") ? atoi(getenv("CD_TC_BN64")) : 1;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
@@ -453,8 +456,8 @@ struct Gemm {
     TcEpiMaps em;
     memset(&em, 0, sizeof(em));
     if (tc_epi_maps(em)) {
-      if (bn == 64) return launch_tc32_k<A_, B_, 1, 4, 64>(units, tm, em);
-      return launch_tc32_k<A_, B_, 1, 4, 128>(units, tm, em);
+      if (bn == 64) return launch_tc32_k<A_, B_, 1, CD_TC_EPI_STG, 64>(units, tm, em);
+      return launch_tc32_k<A_, B_, 1, CD_TC_EPI_STG, 128>(units, tm, em);
     }
     if (bn == 64) return launch_tc32_k<A_, B_, 0, TC_STAGES, 64>(units, tm, em);
     return launch_tc32_k<A_, B_, 0, TC_STAGES, 128>(units, tm, em);

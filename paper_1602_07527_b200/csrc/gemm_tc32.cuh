@@ -129,6 +129,9 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
 constexpr int TCP_THREADS = 192;
 // EPI = 1 adds warp 6: the epilogue's TMA warp (Cin prefetch + output stores).  The last four
 // warps round every operand stage to tf32 in place (cvt.rna) before the MMA reads it.
+#ifndef CD_TC_EPI_MINB
+#define CD_TC_EPI_MINB 1
+#endif
 #ifndef CD_TC_CONVW
 #define CD_TC_CONVW 8
 #endif
@@ -147,7 +150,7 @@ __host__ __device__ constexpr int tcp_threads(int epi) { return (tc_conv_warp0(e
 // STG = depth of the operand ring.  BN = the N tile (128, or 64 for the nb = 64 panels: M x 64
 // products would otherwise issue half-empty MMAs -- the batched forward update is tensor-bound).
 template <int TA, int TB, int EPI, int STG, int BN>
-__global__ void __launch_bounds__(tcp_threads(EPI), EPI ? 1 : CD_TC_MINB)
+__global__ void __launch_bounds__(tcp_threads(EPI), EPI ? CD_TC_EPI_MINB : CD_TC_MINB)
     k_gemm_tc32(const GemmParams p, const __grid_constant__ TmaMaps tm, const __grid_constant__ TcEpiMaps em) {
   constexpr int TC_STAGES = STG;
   constexpr int TC_BN = BN;
