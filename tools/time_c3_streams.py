@@ -33,7 +33,22 @@ def main():
             cd.chol_fwd(Ld, F)
         s_main.wait_stream(s2)
 
-    for name, fn in (("one stream", seq), ("two streams", two), ("one stream", seq), ("two streams", two)):
+    ss = [torch.cuda.Stream() for _ in range(4)]
+
+    def four(parts=2):
+        h = B // parts
+        for x in ss:
+            x.wait_stream(s_main)
+        for i in range(parts):
+            with torch.cuda.stream(ss[2 * i % 4]):
+                cd.chol_rev(Ld[i * h:(i + 1) * h], A[i * h:(i + 1) * h])
+            with torch.cuda.stream(ss[(2 * i + 1) % 4]):
+                cd.chol_fwd(Ld[i * h:(i + 1) * h], F[i * h:(i + 1) * h])
+        for x in ss:
+            s_main.wait_stream(x)
+
+    for name, fn in (("one stream", seq), ("two streams", two), ("four streams (halves)", four),
+                     ("one stream", seq), ("two streams", two), ("four streams (halves)", four)):
         ts = []
         for i in range(7):
             A.copy_(A0)
