@@ -28,6 +28,7 @@
 #include "gemm.cuh"
 #include "gemm_tma.cuh"
 #include "gemm_tc32.cuh"
+#include "symm_tc.cuh"
 #include "misc.cuh"
 #include "sweep_warp.cuh"
 #include "sweep_reg32.cuh"
@@ -927,6 +928,93 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
   }
 }
 
+// ------------------------------------------------------------------ blocked reverse, left-looking, fp32
+// The left-looking schedule of blocked_rev_ll for fp32 on the tcgen05 tensor cores: per block
+// [j, k), right to left,
+//   Cbar <- Cbar - M L[k:n, j:k]         k_symm_tc (stream-K, tf32, in-kernel fixup)
+//   Cbar <- Cbar D^{-1}                  tcgen05 GEMM, in place
+//   Dbar <- Dbar - tril(Cbar^T C)        tcgen05 GEMM, tril
+//   Dbar <- chol_unblocked_rev(D, Dbar)  k_rev_dmma_cta (fp64 arithmetic), + S kept
+// nb = 128, TMA-describable fp32 operands (16-byte aligned, ld % 4 == 0).
+static bool g_no_ll32 = getenv("CD_NO_LL32") != nullptr;
+// pieces per output tile of k_symm_tc (its fixup moves (pieces + 1) fp32 tiles through one SM;
+// 4 measured best: N = 4096 4.13 ms vs 4.41 at 8, N = 16384 31.9 vs 32.2 ms)
+static int64_t g_ll32_pieces = getenv("CD_LL32_PIECES") ? atoi(getenv("CD_LL32_PIECES")) : 4;
+
+static void blocked_rev_ll32(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, float* part_ws) {
+  const int nblk = nblocks(n, nb);
+  float* Dinv = static_cast<float*>(c.take(sizeof(float) * size_t(batch) * nblk * nb * nb));
+  const int64_t s_stride = int64_t(nblk) * 128 * 128;
+  float* Sall = static_cast<float*>(c.take(sizeof(float) * size_t(batch) * s_stride));
+  float* tcpart = static_cast<float*>(c.take(sizeof(float) * size_t(c.sms) * 2 * STC_TILE));
+  int* cnt = static_cast<int*>(c.take(sizeof(int) * size_t(batch) * nblk));
+  if (c.plan || !c.ok()) return;
+  STCMaps tm;
+  memset(&tm, 0, sizeof(tm));
+  tm.batched = batch > 1 ? 1 : 0;
+  {
+    const float* Ab = static_cast<const float*>(A.base) + A.off;
+    const float* Lb = static_cast<const float*>(L.base) + L.off;
+    const bool ok = make_tmap_f32_sw128(&tm.aMN, Ab, n, n, A.ld, A.stride, batch, 32, 32, true) &&
+                    make_tmap_f32_sw128(&tm.aK, Ab, n, n, A.ld, A.stride, batch, 32, 128, false) &&
+                    make_tmap_f32_sw128(&tm.sMN, Sall, 128, int64_t(128) * nblk, 128, s_stride, batch, 32, 32, true) &&
+                    make_tmap_f32_sw128(&tm.lK, Lb, n, n, L.ld, L.stride, batch, 32, 128, false);
+    if (!ok) {
+      c.err = CD_ERR_CUDA;
+      snprintf(g_cuda_err, sizeof(g_cuda_err), "cuTensorMapEncodeTiled failed for the fp32 left-looking sweep");
+      return;
+    }
+  }
+  c.err = note_cuda(cudaMemsetAsync(cnt, 0, sizeof(int) * size_t(batch) * nblk, c.st));
+  set_smem(k_symm_tc, STC_SMEM);
+  run_trinv<float>(c, n, nb, true, batch, L, Dinv);
+  for (int qb = nblk - 1; qb >= 0 && c.ok(); --qb) {
+    int j, w;
+    block_range(n, nb, true, qb, j, w);
+    const int k = j + w, p = n - k;
+    const Opnd Cbar = sub(A, k, j);
+    if (p > 0) {
+      STCParams sp;
+      sp.A = A;
+      sp.n = n, sp.k = k, sp.j = j, sp.w = w;
+      sp.m = p / 128;
+      sp.nblk = nblk;
+      sp.total = batch * int64_t(sp.m) * STC_CHUNKS_PER_BLK * sp.m;
+      // CTAs: >= 2 K chunks each, at most ~PIECES pieces per output tile (see blocked_rev_ll)
+      sp.G = int(std::max<int64_t>(1, std::min<int64_t>({int64_t(c.sms), sp.total / 2,
+                                                         g_ll32_pieces * batch * int64_t(sp.m)})));
+      sp.part = tcpart;
+      sp.cnt = cnt;
+      if (sp.total >= (int64_t(1) << 31)) {
+        c.err = CD_ERR_UNSUPPORTED;
+        return;
+      }
+      c.pre(CD_PROF_SYMM, 2.0 * double(p) * p * w * double(batch));
+      k_symm_tc<<<sp.G, STC_THREADS, STC_SMEM, c.st>>>(sp, tm);
+      c.launched();
+      // Cbar <- Cbar D^{-1}
+      const Opnd Dinv_q = ws_opnd(Dinv + int64_t(qb) * nb * nb, int64_t(nblk) * nb * nb, nb);
+      Gemm<float>(c, p, w, 0, 0, batch)
+          .seg(Cbar, Dinv_q, w)
+          .flops(double(p) * w * (w + 1))
+          .run(null_opnd(), Cbar, 1.0, 0.0, 0, part_ws);
+      // Dbar <- Dbar - tril(Cbar^T C)
+      Gemm<float>(c, w, w, 1, 0, batch)
+          .seg(Cbar, sub(L, k, j), p)
+          .flops(double(w) * (w + 1) * p)
+          .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
+    }
+    // Dbar <- chol_unblocked_rev(D, Dbar); S = Dbar + Dbar^T kept for the later SYMMs
+    const Opnd S = qb > 0 ? ws_opnd(Sall + int64_t(qb) * 128 * 128, s_stride, 128) : null_opnd();
+    run_sweep_small<float>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, S, nullptr);
+  }
+  if (info && c.ok()) {
+    c.pre(CD_PROF_OTHER, 0.0);
+    k_diag_info<float><<<unsigned(batch), 256, 0, c.st>>>(n, L, info);
+    c.launched();
+  }
+}
+
 // ------------------------------------------------------------------ blocked forward
 // chol_blocked_fwd, block [j, k), w = k - j, p = n - k, q = j:
 //   Ddot <- Ddot - tril(Rdot R^T + R Rdot^T)        GEMM (2 K-segments), tril, split-K
@@ -1439,14 +1527,25 @@ static void drive(Ctx& c, const Call& k) {
                                             (reinterpret_cast<uintptr_t>(static_cast<const double*>(k.L.base) + k.L.off) % 16) == 0 &&
                                             k.A.ld % 2 == 0 && k.L.ld % 2 == 0 &&
                                             (k.batch == 1 || (k.A.stride % 2 == 0 && k.L.stride % 2 == 0))));
+    // fp32 left-looking schedule (single matrices: batches keep the right-looking sweep, whose
+    // nb = 64 diagonal blocks are cheaper -- DESIGN.md §9)
+    const bool ll32_shape = k.dt == CD_F32 && nb == 128 && k.batch == 1 && n >= 1024 && !g_no_ll32 &&
+                            !g_tma_disabled && !g_tc32_disabled && !k.L.arr && !k.A.arr;
+    const bool ll32 = ll32_shape && (c.plan || ((reinterpret_cast<uintptr_t>(static_cast<const float*>(k.A.base) + k.A.off) % 16) == 0 &&
+                                                (reinterpret_cast<uintptr_t>(static_cast<const float*>(k.L.base) + k.L.off) % 16) == 0 &&
+                                                k.A.ld % 4 == 0 && k.L.ld % 4 == 0));
     const size_t o0 = c.off;
     size_t o_ll = o0;
     if (ll) {
       blocked_rev_ll(c, n, nb, k.batch, k.L, k.A, k.info, reinterpret_cast<double*>(part));
       o_ll = c.off;
       c.off = o0;
+    } else if (ll32) {
+      blocked_rev_ll32(c, n, nb, k.batch, k.L, k.A, k.info, reinterpret_cast<float*>(part));
+      o_ll = c.off;
+      c.off = o0;
     }
-    if (!ll || c.plan) {
+    if (!(ll || ll32) || c.plan) {
       // lookahead schedule needs a one-tile-wide block (in-place panel solve) and library streams
       T* part2 = static_cast<T*>(c.take(sizeof(T) * size_t(PART_TILES) * G_BM * G_BN));
       // (batches already fill the GPU: the lookahead's extra launches only cost there)

@@ -267,6 +267,19 @@ def test_f32_blocked_sizes(n, B):
     assert nerr(to_host(f), oracle_fwd(L, Sd)) < TOL32
 
 
+@pytest.mark.parametrize("n", [1024, 1100, 1537])
+def test_f32_left_looking_nan_upper(n):
+    # fp32 single matrices n >= 1024 take the left-looking tcgen05 schedule (k_symm_tc): the upper
+    # triangles (NaN here) must never be read, ragged top-left block included
+    L, Lb, _ = synthetic.draw(n, 61 + n)
+    L, Lb = fp32_round(L, Lb)
+    nan_up = np.triu(np.full((n, n), np.nan), 1)
+    r = cd.chol_rev(to_dev(L + nan_up, torch.float32), to_dev(Lb + nan_up, torch.float32))
+    out = to_host(r)
+    assert np.all(np.isnan(np.triu(out, 1)[np.triu_indices(n, 1)]))  # upper never written
+    assert nerr(out, oracle.chol_rev(L, Lb)) < 2.5e-5
+
+
 @pytest.mark.parametrize("n,B,dt", [(300, 3, torch.float64), (512, 2, torch.float32), (40, 5, torch.float64)])
 def test_rev_fwd_two_streams_equal_separate_calls(n, B, dt):
     L, Lb, Sd = synthetic.draw_batch(n, B, seed=8 * n, sdot=True)
