@@ -130,6 +130,19 @@ int cd_chol_fwd_batched(cd_dtype dt, int64_t n, const void* const* L_array, int6
                         void* const* Adot_array, int64_t ldadot, int64_t batch, const cd_opts* opts,
                         void* ws, size_t ws_bytes, int* d_info, cd_stream_t stream);
 
+/* Both sensitivities of the same factors in one call (configs[3]'s workload): Abar (tril(Lbar) ->
+ * tril(Sigma_bar), per opts->out_mode) and Adot (tril(Sigma_dot) -> L_dot), i.e. cd_chol_rev and
+ * cd_chol_fwd on the same L.  The two sweeps are independent; the forward one runs on a
+ * library-owned stream (per device and host thread) that starts after the work already queued on
+ * `stream` and that `stream` waits for, so the call is ordered on `stream` like any other.
+ * d_info (optional) receives the reverse sweep's status.  Argument checks as for the strided
+ * batched calls (1-based positions); ws >= cd_workspace_size_rev_fwd(...) bytes (-14 otherwise). */
+size_t cd_workspace_size_rev_fwd(cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts);
+int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t strideL,
+                                    void* Abar, int64_t ldabar, int64_t strideAbar, void* Adot, int64_t ldadot,
+                                    int64_t strideAdot, int64_t batch, const cd_opts* opts, void* ws,
+                                    size_t ws_bytes, int* d_info, cd_stream_t stream);
+
 /* Device workspace (bytes) that a call with these arguments needs; 0 if none.
  * `batch` = 1 for the single-matrix calls.  For the pointer-array batched calls
  * pass the batch size as well. */

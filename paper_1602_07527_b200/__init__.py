@@ -96,6 +96,11 @@ def lib():
             L.cd_dist_fwd_partial.restype = ctypes.c_int
             L.cd_dist_fwd_panel.argtypes = [ctypes.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp]
             L.cd_dist_fwd_panel.restype = ctypes.c_int
+            L.cd_workspace_size_rev_fwd.argtypes = [ctypes.c_int, i64, i64, po]
+            L.cd_workspace_size_rev_fwd.restype = sz
+            L.cd_chol_rev_fwd_strided_batched.argtypes = [ctypes.c_int, i64, vp, i64, i64, vp, i64, i64, vp, i64,
+                                                          i64, i64, po, vp, sz, vp, vp]
+            L.cd_chol_rev_fwd_strided_batched.restype = ctypes.c_int
             L.cd_status_string.argtypes = [ctypes.c_int]
             L.cd_status_string.restype = ctypes.c_char_p
             L.cd_last_cuda_error.restype = ctypes.c_char_p
@@ -236,29 +241,35 @@ def chol_fwd(L: torch.Tensor, Sdot: torch.Tensor, *, nb=None, route: str = "auto
     return _run(CD_OP_FWD, L, A, nb, route, "tril", info)
 
 
-_side_streams: dict = {}
-
-
 def chol_rev_fwd(L: torch.Tensor, Lbar: torch.Tensor, Sdot: torch.Tensor, *, nb=None, inplace: bool = True):
-    """Both sensitivities of one factor (configs[3]'s workload): Sigma_bar = chol_rev(L, Lbar) on the
-    current stream and L_dot = chol_fwd(L, Sdot) on a side stream, joined back into the current
-    stream before returning.  The two sweeps are independent, so their latency-bound diagonal-block
-    launches fill the gaps of each other's bandwidth-bound updates.  Returns (Sigma_bar, L_dot)."""
-    dev = Lbar.device
-    cur = torch.cuda.current_stream(dev)
-    side = _side_streams.get(dev.index)
-    if side is None:
-        side = _side_streams[dev.index] = torch.cuda.Stream(dev)
+    """Both sensitivities of one factor (configs[3]'s workload) in one library call
+    (cd_chol_rev_fwd_strided_batched): Sigma_bar = chol_rev(L, Lbar) and L_dot = chol_fwd(L, Sdot),
+    the two independent sweeps on two streams inside the library, ordered on the current stream.
+    Returns (Sigma_bar, L_dot)."""
     Lc, A = _prep(L, Lbar, inplace)
     _, F = _prep(Lc, Sdot, inplace)
-    side.wait_stream(cur)
-    r = _run(CD_OP_REV, Lc, A, nb, "auto", "tril", False)
-    with torch.cuda.stream(side):
-        f = _run(CD_OP_FWD, Lc, F, nb, "auto", "tril", False)
-    cur.wait_stream(side)
-    for t in (Lc, F):
-        t.record_stream(side)
-    return r, f
+    if F.shape != A.shape or F.dtype != A.dtype:
+        raise ValueError("Lbar and Sdot must match")
+    Lk = lib()
+    n = A.shape[-1]
+    batch = A.shape[0] if A.dim() == 3 else 1
+    if n == 0 or batch == 0:
+        return A, F
+    o = _opts(nb, "auto", "tril")
+    dt = _dt(A)
+    dev = A.device
+    with torch.cuda.device(dev):
+        nbytes = int(Lk.cd_workspace_size_rev_fwd(dt, n, batch, ctypes.byref(o)))
+        ws = _workspace(nbytes, dev)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        ld = lambda t: max(1, t.stride(-1)) if n > 1 else 1  # noqa: E731
+        sb = lambda t: (t.stride(0) if batch > 1 else ld(t) * n) if t.dim() == 3 else ld(t) * n  # noqa: E731
+        wsp = ctypes.c_void_p(ws.data_ptr()) if ws is not None else None
+        rc = Lk.cd_chol_rev_fwd_strided_batched(dt, n, Lc.data_ptr(), ld(Lc), sb(Lc), A.data_ptr(), ld(A), sb(A),
+                                                F.data_ptr(), ld(F), sb(F), batch, ctypes.byref(o), wsp, nbytes,
+                                                None, stream)
+        _check(rc)
+    return A, F
 
 
 def chol_fwd_fused(Sigma: torch.Tensor, Sdot: torch.Tensor, *, info: bool = False):

@@ -1849,12 +1849,77 @@ int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t l
                  stream, false);
 }
 
+// ---- both sweeps of one factor on two streams (cd_chol_rev_fwd_strided_batched) ----
+static thread_local cudaStream_t g_side[64];
+static thread_local std::vector<cudaEvent_t> g_side_ev[64];
+
+static size_t rev_fwd_ws(cd_dtype dt, int64_t n, int64_t batch, const cd_opts& o, size_t* ws_rev) {
+  Call kr{CD_OP_REV, dt, n, batch, null_opnd(), null_opnd(), o, nullptr};
+  kr.L.ld = kr.A.ld = n;
+  Call kf = kr;
+  kf.op = CD_OP_FWD;
+  kf.o.out_mode = CD_OUT_TRIL;
+  const size_t a = (plan_size(kr) + 255) & ~size_t(255);
+  if (ws_rev) *ws_rev = a;
+  return a + plan_size(kf);
+}
+
 size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts) {
   if ((dt != CD_F64 && dt != CD_F32) || n <= 0 || batch <= 0) return 0;
   const cd_opts o = opts ? *opts : kDefaultOpts;
   Call k{op, dt, n, batch, null_opnd(), null_opnd(), o, nullptr};
   k.L.ld = k.A.ld = n;
   return plan_size(k);
+}
+
+size_t cd_workspace_size_rev_fwd(cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts) {
+  if ((dt != CD_F64 && dt != CD_F32) || n <= 0 || batch <= 0) return 0;
+  const cd_opts o = opts ? *opts : kDefaultOpts;
+  return rev_fwd_ws(dt, n, batch, o, nullptr);
+}
+
+int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t strideL, void* Abar,
+                                    int64_t ldabar, int64_t strideAbar, void* Adot, int64_t ldadot,
+                                    int64_t strideAdot, int64_t batch, const cd_opts* opts, void* ws,
+                                    size_t ws_bytes, int* d_info, cd_stream_t stream) {
+  int r = check_common(CD_OP_REV, dt, n, ldl, ldabar, opts, 1, 2, 4, 7, 13);
+  if (r) return r;
+  if (ldadot < std::max<int64_t>(1, n)) return -10;
+  if (batch < 0) return -12;
+  if (n == 0 || batch == 0) return CD_SUCCESS;
+  if (!L) return -3;
+  if (!Abar) return -6;
+  if (!Adot) return -9;
+  if (batch > 1 && (strideL < ldl * n)) return -5;
+  if (batch > 1 && (strideAbar < ldabar * n)) return -8;
+  if (batch > 1 && (strideAdot < ldadot * n)) return -11;
+  const cd_opts o = opts ? *opts : kDefaultOpts;
+  size_t ws_rev = 0;
+  const size_t need = rev_fwd_ws(dt, n, batch, o, &ws_rev);
+  if (need > 0 && (!ws || ws_bytes < need)) return -14;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CD_ERR_CUDA;
+  if (!g_side[dev] && (r = note_cuda(cudaStreamCreateWithFlags(&g_side[dev], cudaStreamNonBlocking)))) return r;
+  std::vector<cudaEvent_t>& evs = g_side_ev[dev];
+  if (evs.empty()) {
+    evs.resize(2);
+    for (auto& e : evs)
+      if ((r = note_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)))) return r;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream), side = g_side[dev];
+  // the side stream starts after the work already queued on `stream`, and `stream` ends after it
+  if ((r = note_cuda(cudaEventRecord(evs[0], st)))) return r;
+  if ((r = note_cuda(cudaStreamWaitEvent(side, evs[0], 0)))) return r;
+  Call kr{CD_OP_REV, dt, n, batch, Opnd{L, nullptr, strideL, ldl, 0}, Opnd{Abar, nullptr, strideAbar, ldabar, 0}, o,
+          d_info};
+  Call kf{CD_OP_FWD, dt, n, batch, Opnd{L, nullptr, strideL, ldl, 0}, Opnd{Adot, nullptr, strideAdot, ldadot, 0}, o,
+          nullptr};
+  kf.o.out_mode = CD_OUT_TRIL;
+  r = execute(kr, ws, ws_rev, st, 14);
+  const int rf = execute(kf, static_cast<char*>(ws) + ws_rev, ws_bytes - ws_rev, side, 14);
+  const int rj = note_cuda(cudaEventRecord(evs[1], side));
+  const int rw = rj ? rj : note_cuda(cudaStreamWaitEvent(st, evs[1], 0));
+  return r ? r : (rf ? rf : rw);
 }
 
 size_t cd_workspace_size_host(cd_op op, cd_dtype dt, int64_t n, const cd_opts* opts) {
