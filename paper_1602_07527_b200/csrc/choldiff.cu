@@ -313,6 +313,9 @@ static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
 #ifndef CD_TC_EPI_STG
 #define CD_TC_EPI_STG 4
 #endif
+#ifndef CD_TC_EPI_STG64  // 64-wide tiles: 24 KB stages, so a deeper ring fits beside the epilogue slots
+#define CD_TC_EPI_STG64 5
+#endif
 static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
 static int g_tc_bn64 = getenv("CD_TC_BN64") ? atoi(getenv("CD_TC_BN64")) : 1;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
@@ -457,7 +460,7 @@ struct Gemm {
     TcEpiMaps em;
     memset(&em, 0, sizeof(em));
     if (tc_epi_maps(em)) {
-      if (bn == 64) return launch_tc32_k<A_, B_, 1, CD_TC_EPI_STG, 64>(units, tm, em);
+      if (bn == 64) return launch_tc32_k<A_, B_, 1, CD_TC_EPI_STG64, 64>(units, tm, em);
       return launch_tc32_k<A_, B_, 1, CD_TC_EPI_STG, 128>(units, tm, em);
     }
     if (bn == 64) return launch_tc32_k<A_, B_, 0, TC_STAGES, 64>(units, tm, em);
@@ -644,6 +647,16 @@ static void run_sym2(Ctx& c, int n, int64_t batch, Opnd A, Opnd S, int clean) {
 // W is written straight into Abar's Cbar region when one 128-wide N-tile covers
 // the block (each CTA then reads its rows completely before writing them);
 // otherwise through workspace + copy.
+// cd_chol_rev_fwd: the diagonal-block inverses of the shared factor, made once for both sweeps
+// (valid when both partitions coincide, n % nb == 0; set only around that call's two enqueues)
+static thread_local const void* g_ext_dinv = nullptr;
+static thread_local int g_ext_dinv_nb = 0;
+
+template <typename T>
+static T* shared_dinv(int n, int nb) {
+  return (g_ext_dinv && g_ext_dinv_nb == nb && n % nb == 0) ? static_cast<T*>(const_cast<void*>(g_ext_dinv)) : nullptr;
+}
+
 template <typename T>
 static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, T* part_ws) {
   const int nblk = nblocks(n, nb);
@@ -651,7 +664,8 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
   T* Sws = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nb * nb));
   const bool w_inplace = nb <= G_BN;
   T* Wws = w_inplace ? nullptr : static_cast<T*>(c.take(sizeof(T) * size_t(batch) * n * nb));
-  run_trinv<T>(c, n, nb, true, batch, L, Dinv);
+  if (T* ext = shared_dinv<T>(n, nb)) Dinv = c.plan ? Dinv : ext;
+  else run_trinv<T>(c, n, nb, true, batch, L, Dinv);
   for (int qb = nblk - 1; qb >= 0; --qb) {
     int j, w;
     block_range(n, nb, true, qb, j, w);
@@ -1030,7 +1044,8 @@ static void blocked_fwd(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
   T* Dcw = static_cast<T*>(c.take(sizeof(T) * size_t(batch) * nb * nb));
   const bool w_inplace = nb <= G_BN;  // see blocked_rev
   T* Wws = w_inplace ? nullptr : static_cast<T*>(c.take(sizeof(T) * size_t(batch) * n * nb));
-  run_trinv<T>(c, n, nb, false, batch, L, Dinv);
+  if (T* ext = shared_dinv<T>(n, nb)) Dinv = c.plan ? Dinv : ext;
+  else run_trinv<T>(c, n, nb, false, batch, L, Dinv);
   for (int qb = 0; qb < nblk; ++qb) {
     int j, w;
     block_range(n, nb, false, qb, j, w);
@@ -1853,15 +1868,27 @@ int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t l
 static thread_local cudaStream_t g_side[64];
 static thread_local std::vector<cudaEvent_t> g_side_ev[64];
 
-static size_t rev_fwd_ws(cd_dtype dt, int64_t n, int64_t batch, const cd_opts& o, size_t* ws_rev) {
+// the batched fp32 right-looking drivers share one set of diagonal-block inverses (configs[3])
+static int shared_dinv_nb(cd_dtype dt, int64_t n, int64_t batch, const cd_opts& o) {
+  const int nb = int(std::min<int64_t>(n, o.nb > 0 ? o.nb : default_nb(dt, n)));
+  const bool ok = dt == CD_F32 && batch > 1 && n > DC_NMAX && nb <= DC_NMAX && n % nb == 0 &&
+                  o.route != CD_ROUTE_SYMBOLIC;
+  return ok ? nb : 0;
+}
+
+static size_t rev_fwd_ws(cd_dtype dt, int64_t n, int64_t batch, const cd_opts& o, size_t* ws_rev, size_t* ws_dinv) {
   Call kr{CD_OP_REV, dt, n, batch, null_opnd(), null_opnd(), o, nullptr};
   kr.L.ld = kr.A.ld = n;
   Call kf = kr;
   kf.op = CD_OP_FWD;
   kf.o.out_mode = CD_OUT_TRIL;
   const size_t a = (plan_size(kr) + 255) & ~size_t(255);
+  const size_t f = (plan_size(kf) + 255) & ~size_t(255);
   if (ws_rev) *ws_rev = a;
-  return a + plan_size(kf);
+  if (ws_dinv) *ws_dinv = a + f;
+  const int nb = shared_dinv_nb(dt, n, batch, o);
+  const size_t es = dt == CD_F64 ? 8 : 4;
+  return a + f + (nb ? size_t(batch) * (n / nb) * nb * nb * es : 0);
 }
 
 size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts) {
@@ -1875,7 +1902,7 @@ size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const 
 size_t cd_workspace_size_rev_fwd(cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts) {
   if ((dt != CD_F64 && dt != CD_F32) || n <= 0 || batch <= 0) return 0;
   const cd_opts o = opts ? *opts : kDefaultOpts;
-  return rev_fwd_ws(dt, n, batch, o, nullptr);
+  return rev_fwd_ws(dt, n, batch, o, nullptr, nullptr);
 }
 
 int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64_t ldl, int64_t strideL, void* Abar,
@@ -1894,8 +1921,8 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
   if (batch > 1 && (strideAbar < ldabar * n)) return -8;
   if (batch > 1 && (strideAdot < ldadot * n)) return -11;
   const cd_opts o = opts ? *opts : kDefaultOpts;
-  size_t ws_rev = 0;
-  const size_t need = rev_fwd_ws(dt, n, batch, o, &ws_rev);
+  size_t ws_rev = 0, ws_dinv = 0;
+  const size_t need = rev_fwd_ws(dt, n, batch, o, &ws_rev, &ws_dinv);
   if (need > 0 && (!ws || ws_bytes < need)) return -14;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CD_ERR_CUDA;
@@ -1907,6 +1934,19 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
       if ((r = note_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)))) return r;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream), side = g_side[dev];
+  const int snb = shared_dinv_nb(dt, n, batch, o);
+  if (snb) {  // the inverses of the shared factor, once, before the two sweeps fork
+    Ctx c;
+    c.plan = false;
+    c.ws = nullptr;
+    c.st = st;
+    c.sms = sm_count();
+    float* Dinv = reinterpret_cast<float*>(static_cast<char*>(ws) + ws_dinv);
+    run_trinv<float>(c, int(n), snb, false, batch, Opnd{L, nullptr, strideL, ldl, 0}, Dinv);
+    if (c.err) return c.err;
+    g_ext_dinv = Dinv;
+    g_ext_dinv_nb = snb;
+  }
   // the side stream starts after the work already queued on `stream`, and `stream` ends after it
   if ((r = note_cuda(cudaEventRecord(evs[0], st)))) return r;
   if ((r = note_cuda(cudaStreamWaitEvent(side, evs[0], 0)))) return r;
@@ -1916,7 +1956,9 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
           nullptr};
   kf.o.out_mode = CD_OUT_TRIL;
   r = execute(kr, ws, ws_rev, st, 14);
-  const int rf = execute(kf, static_cast<char*>(ws) + ws_rev, ws_bytes - ws_rev, side, 14);
+  const int rf = execute(kf, static_cast<char*>(ws) + ws_rev, ws_dinv - ws_rev, side, 14);
+  g_ext_dinv = nullptr;
+  g_ext_dinv_nb = 0;
   const int rj = note_cuda(cudaEventRecord(evs[1], side));
   const int rw = rj ? rj : note_cuda(cudaStreamWaitEvent(st, evs[1], 0));
   return r ? r : (rf ? rf : rw);
