@@ -1156,6 +1156,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pf.T0 = A;
     pf.single = 0;
     pf.skip3 = 0;
+    pf.dbg_skip = g_dbg_panel_skip;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
     void* args[] = {&pf};
     const double wf = w;
@@ -1296,6 +1297,7 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
       pf.kchunks = q / 128;
       pf.single = 1;
       pf.skip3 = 1;
+      pf.dbg_skip = 0;
       panel(pf, double(p_prev) * 128 * 129 + double(w) * (w + 1) * q);
     }
     // D <- chol_unblocked(D), D^{-1}

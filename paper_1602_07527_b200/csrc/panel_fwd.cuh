@@ -40,6 +40,7 @@ struct PanelFwdParams {
   Opnd T0;               // phase-0 target matrix (W <- W D^{-T} in place); the forward sweep: A
   int single;            // phase 1: one product R R^T (K = 128 per chunk) instead of both
   int skip3;             // skip phase 3 (Eq. 8)
+  int dbg_skip;          // measurement only (CD_DEBUG_PANEL_SKIP): bit i skips phase i; results wrong
 };
 
 // acc (64 x 32 warp tiles of a 128 x 128 tile) += sum over K of A(m, kk) B(kk, c), K in
@@ -108,7 +109,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   // ---------------- phase 0: previous panel  Cdot <- W D_prev^{-T} ----------------
   // 32 x 32 output tiles (16 per 128-row tile), so small panels still spread over the GPU
   const bool big0 = p.batch * p.tiles_prev >= int64_t(gridDim.x) / 2;
-  if (p.Dinv_prev && big0) {  // one CTA per 128-row tile
+  const bool ph0 = p.Dinv_prev && !(p.dbg_skip & 1);
+  if (ph0 && big0) {  // one CTA per 128-row tile
     const int lane_ = threadIdx.x & 31, wm = warp >> 2, wn = warp & 3, g = lane_ >> 2, t = lane_ & 3;
     const int64_t units = p.batch * p.tiles_prev;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
     }
     __threadfence();
     cg::this_grid().sync();
-  } else if (p.Dinv_prev) {
+  } else if (ph0) {
     const int64_t units = p.batch * p.tiles_prev * 16;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int64_t bt = u >> 4;
@@ -182,15 +184,16 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   }
 
   // ---------------- phase 1: partials of Rdot R^T + R Rdot^T ----------------
+  const int kch1 = (p.dbg_skip & 2) ? 0 : p.kchunks;
   // unit = (128-wide K chunk, lower 32 x 32 tile of the w x w block): K = 256 (both
   // products); with enough K chunks, one CTA per chunk computes the whole 128 x 128 block
-  const bool big1 = p.batch * p.kchunks >= int64_t(gridDim.x) / 2;
+  const bool big1 = p.batch * kch1 >= int64_t(gridDim.x) / 2;
   if (big1) {
     const int lane_ = threadIdx.x & 31, wm = warp >> 2, wn = warp & 3, g = lane_ >> 2, t = lane_ & 3;
-    const int64_t units = p.batch * p.kchunks;
+    const int64_t units = p.batch * kch1;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const int64_t b = u / p.kchunks;
-      const int kc0 = 128 * int(u - b * p.kchunks);
+      const int64_t b = u / kch1;
+      const int kc0 = 128 * int(u - b * kch1);
       const double* Ad = optr<double>(p.A, b) + p.j + int64_t(kc0) * p.A.ld;
       const double* Lr = optr<double>(p.L, b) + p.j + int64_t(kc0) * p.L.ld;
       double acc[8][4][2];
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
           }
     }
   } else {
-    const int64_t units = p.batch * p.kchunks * 10;
+    const int64_t units = p.batch * kch1 * 10;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int64_t bk = u / 10;
       const int lt = int(u - bk * 10);
@@ -232,8 +235,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
         while (r > ti) r -= ++ti;
         tj = r;
       }
-      const int64_t b = bk / p.kchunks;
-      const int kc0 = 128 * int(bk - b * p.kchunks);
+      const int64_t b = bk / kch1;
+      const int kc0 = 128 * int(bk - b * kch1);
       const double* Ad = optr<double>(p.A, b) + p.j + int64_t(kc0) * p.A.ld;  // Rdot chunk, rows j..
       const double* Lr = optr<double>(p.L, b) + p.j + int64_t(kc0) * p.L.ld;  // R chunk
       const int a0 = 32 * ti, c0 = 32 * tj;
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   cg::this_grid().sync();
 
   // ---------------- phase 2: Ddot -= sum of the partials (lower triangle) ----------------
-  if (p.kchunks > 0) {
+  if (p.kchunks > 0 && !(p.dbg_skip & 4)) {
     const int64_t nwarps = int64_t(gridDim.x) * (PR_THREADS / 32);
     const int64_t gw = int64_t(blockIdx.x) * (PR_THREADS / 32) + warp;
     const int64_t ntri = int64_t(w) * (w + 1) / 2;
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   }
 
   // ---------------- phase 3: Ldot_D = D Phi(D^{-1} Ddot_sym D^{-T})  (Eq. 8) ----------------
-  const int64_t u3 = p.skip3 ? 0 : p.batch * 16;
+  const int64_t u3 = (p.skip3 || (p.dbg_skip & 8)) ? 0 : p.batch * 16;
   // 3a: Y = D^{-1} X,  X(r, c) = Ddot(max, min)
   for (int64_t u = blockIdx.x; u < u3; u += gridDim.x) {
     const int64_t b = u >> 4;
