@@ -407,3 +407,48 @@ def test_cuda_graph_capture_and_replay(n, B, dt):
         g.replay()
     torch.cuda.synchronize()
     assert nerr(to_host(A), oracle_rev(L, Lb)) < (TOL64 if dt == torch.float64 else TOL32)
+
+
+@pytest.mark.parametrize("n,B,dt", [(512, 4, torch.float32), (300, 2, torch.float64)])
+def test_rev_fwd_cuda_graph_and_info(n, B, dt):
+    # cd_chol_rev_fwd forks the forward sweep onto a library stream and joins it back: the call can
+    # be captured into a CUDA graph; d_info carries the reverse sweep's status (a zero pivot)
+    L, Lb, Sd = synthetic.draw_batch(n, B, seed=91 + n, sdot=True)
+    if dt == torch.float32:
+        L, Lb, Sd = fp32_round(L, Lb, Sd)
+    Ld, A0, F0 = to_dev(L, dt), to_dev(Lb, dt), to_dev(np.tril(Sd), dt)
+    A, F = A0.clone(), F0.clone()
+    cd.chol_rev_fwd(Ld, A, F)  # warm-up outside capture (library streams and events)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cd.chol_rev_fwd(Ld, A, F)
+    for _ in range(2):
+        A.copy_(A0)
+        F.copy_(F0)
+        g.replay()
+    torch.cuda.synchronize()
+    tol = TOL64 if dt == torch.float64 else 2.5e-5
+    Ah, Fh = to_host(A), to_host(F)
+    for b in range(B):
+        assert nerr(Ah[b], oracle.chol_rev(L[b], Lb[b])) < tol
+        assert nerr(Fh[b], oracle.chol_fwd(L[b], np.tril(Sd[b]))) < tol
+    # d_info through the C ABI: a zero pivot in matrix 1 at 1-based index 5
+    Lz = L.copy()
+    Lz[1, 4, 4] = 0.0
+    Lzd = to_dev(Lz, dt)
+    A2, F2 = A0.clone(), F0.clone()
+    info = torch.zeros(B, dtype=torch.int32, device="cuda")
+    Lk = cd.lib()
+    o = cd._opts(None, "auto", "tril")
+    dtc = cd.CD_F64 if dt == torch.float64 else cd.CD_F32
+    nbytes = int(Lk.cd_workspace_size_rev_fwd(dtc, n, B, ctypes.byref(o)))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+    rc = Lk.cd_chol_rev_fwd_strided_batched(dtc, n, Lzd.data_ptr(), n, n * n, A2.data_ptr(), n, n * n, F2.data_ptr(),
+                                            n, n * n, B, ctypes.byref(o), ws.data_ptr(), nbytes,
+                                            ctypes.c_void_p(info.data_ptr()),
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    got = info.cpu().tolist()
+    assert got[1] == 5 and all(v == 0 for i, v in enumerate(got) if i != 1)
