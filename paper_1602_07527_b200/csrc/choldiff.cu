@@ -811,6 +811,7 @@ static int64_t g_ll_pieces = getenv("CD_LL_PIECES") ? atoi(getenv("CD_LL_PIECES"
 // the SYMM moves into the panel kernel while its 32 x 32 output tiles number <= this x #SMs
 static int64_t g_symm_in_panel = getenv("CD_SYMM_IN_PANEL") ? atoi(getenv("CD_SYMM_IN_PANEL")) : 1;
 static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DEBUG_PANEL_SKIP")) : 0;
+static bool g_no_bal1 = getenv("CD_NO_BAL1") != nullptr;  // forward panel: one CTA per 128-wide K chunk
 
 static int panel_occupancy() {
   static int occ = 0;
@@ -1099,7 +1100,9 @@ static int panel_fwd_occupancy() {
 static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info) {
   const int nblk = nblocks(n, nb);
   double* Dinv = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * nb * nb));
-  double* part = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
+  // phase-1 partial slots: nblk per matrix, or one per SM for single matrices (balanced K split)
+  const int kslots = batch == 1 ? std::max(nblk, c.sms) : nblk;
+  double* part = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * kslots * 128 * 128));
   double* Yws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   double* Fws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   double* Dc = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 132 * 128));
@@ -1157,6 +1160,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pf.single = 0;
     pf.skip3 = 0;
     pf.dbg_skip = g_dbg_panel_skip;
+    pf.kslot_cap = g_no_bal1 ? 0 : kslots;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
     void* args[] = {&pf};
     const double wf = w;
@@ -1211,7 +1215,9 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
 static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad, int* info) {
   const int nblk = nblocks(n, nb);
   double* Dinv = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * nb * nb));
-  double* part = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
+  // phase-1 partial slots: nblk per matrix, or one per SM for single matrices (balanced K split)
+  const int kslots = batch == 1 ? std::max(nblk, c.sms) : nblk;
+  double* part = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * kslots * 128 * 128));
   double* Yws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   double* Fws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   double* Dc = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 132 * 128));
@@ -1278,6 +1284,7 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
     pf.Yws = Yws;
     pf.Fws = Fws;
     pf.Dc = Dc;
+    pf.kslot_cap = g_no_bal1 ? 0 : kslots;
   };
   int j_prev = 0, k_prev = 0, p_prev = 0;
   for (int qb = 0; qb < nblk && c.ok(); ++qb) {

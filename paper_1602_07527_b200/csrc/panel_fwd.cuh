@@ -41,6 +41,7 @@ struct PanelFwdParams {
   int single;            // phase 1: one product R R^T (K = 128 per chunk) instead of both
   int skip3;             // skip phase 3 (Eq. 8)
   int dbg_skip;          // measurement only (CD_DEBUG_PANEL_SKIP): bit i skips phase i; results wrong
+  int kslot_cap;         // phase 1 partial slots available per batch entry (balanced K split, batch 1)
 };
 
 // acc (64 x 32 warp tiles of a 128 x 128 tile) += sum over K of A(m, kk) B(kk, c), K in
@@ -188,7 +189,51 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   // unit = (128-wide K chunk, lower 32 x 32 tile of the w x w block): K = 256 (both
   // products); with enough K chunks, one CTA per chunk computes the whole 128 x 128 block
   const bool big1 = p.batch * kch1 >= int64_t(gridDim.x) / 2;
-  if (big1) {
+  // single matrix with many K chunks: every CTA takes one balanced K range (a multiple of 16
+  // columns) of the whole 128 x 128 block instead of one 128-wide chunk, so all SMs share the
+  // work (kchunks < #SMs left the rest idle); its partial goes to slot blockIdx.x
+  const int gk = min(int(gridDim.x), p.kslot_cap);
+  const bool bal1 = big1 && p.batch == 1 && gk >= kch1;
+  const int nslot1 = bal1 ? gk : kch1;  // phase 1 partial slots per batch entry (phase 2 sums them)
+  if (bal1) {
+    const int lane_ = threadIdx.x & 31, wm = warp >> 2, wn = warp & 3, g = lane_ >> 2, t = lane_ & 3;
+    const int q16 = (128 * kch1) / 16;  // K in 16-column groups
+    for (int u = blockIdx.x; u < gk; u += gridDim.x) {
+      const int k_lo = 16 * int(int64_t(q16) * u / gk), k_hi = 16 * int(int64_t(q16) * (u + 1) / gk);
+      const int kw = k_hi - k_lo;
+      double acc[8][4][2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+      if (kw > 0) {
+        const double* Ad = optr<double>(p.A, 0) + p.j + int64_t(k_lo) * p.A.ld;
+        const double* Lr = optr<double>(p.L, 0) + p.j + int64_t(k_lo) * p.L.ld;
+        pf_prod128(
+            sm, p.single ? kw : 2 * kw,
+            [&](int m, int kk) -> const double* {
+              if (m >= w) return nullptr;
+              return kk < kw ? Ad + m + int64_t(kk) * p.A.ld : Lr + m + int64_t(kk - kw) * p.L.ld;
+            },
+            [&](int kk, int c) -> const double* {
+              if (c >= w) return nullptr;
+              return kk < kw ? Lr + c + int64_t(kk) * p.L.ld : Ad + c + int64_t(kk - kw) * p.A.ld;
+            },
+            [&](int) { return wm * 64 + 63 < wn * 32; },  // warp tile entirely above the diagonal
+            acc);
+      }
+      double* slot = p.part + int64_t(u) * (128 * 128);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = wm * 64 + i * 8 + g, c = wn * 32 + jj * 8 + 2 * t + e;
+            if (r >= c) __stcg(slot + r + c * 128, acc[i][jj][e]);
+          }
+    }
+  } else if (big1) {
     const int lane_ = threadIdx.x & 31, wm = warp >> 2, wn = warp & 3, g = lane_ >> 2, t = lane_ & 3;
     const int64_t units = p.batch * kch1;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -287,17 +332,17 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       }
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       if (on) {
-        const double* pb = p.part + b * p.kchunks * int64_t(128 * 128) + a + c * 128;
+        const double* pb = p.part + b * nslot1 * int64_t(128 * 128) + a + c * 128;
         constexpr int64_t TS = 128 * 128;
         int tl = q;
-        for (; tl + 24 < p.kchunks; tl += 32) {
+        for (; tl + 24 < nslot1; tl += 32) {
           const double x0 = __ldcg(pb + tl * TS), x1 = __ldcg(pb + (tl + 8) * TS);
           const double x2 = __ldcg(pb + (tl + 16) * TS), x3 = __ldcg(pb + (tl + 24) * TS);
           s0 += x0, s1 += x1, s2 += x2, s3 += x3;
         }
-        if (tl < p.kchunks) s0 += __ldcg(pb + tl * TS);
-        if (tl + 8 < p.kchunks) s1 += __ldcg(pb + (tl + 8) * TS);
-        if (tl + 16 < p.kchunks) s2 += __ldcg(pb + (tl + 16) * TS);
+        if (tl < nslot1) s0 += __ldcg(pb + tl * TS);
+        if (tl + 8 < nslot1) s1 += __ldcg(pb + (tl + 8) * TS);
+        if (tl + 16 < nslot1) s2 += __ldcg(pb + (tl + 16) * TS);
       }
       double s = (s0 + s1) + (s2 + s3);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
