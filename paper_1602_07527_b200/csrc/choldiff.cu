@@ -352,6 +352,11 @@ struct Gemm {
     algo_flops = f;
     return *this;
   }
+  // store D (and read Cin) transposed: the user's D is N x M (fp32 tcgen05 TMA epilogue only)
+  Gemm& trans_out() {
+    p.dtrans = 1;
+    return *this;
+  }
   // D = alpha * sum + beta * Cin
   void run(Opnd Cin, Opnd D, double alpha, double beta, int tril, T* part_ws) {
     if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
@@ -370,7 +375,7 @@ struct Gemm {
     p.tril = tril;  // 0 none; 1 + offset (see GemmParams)
     const int64_t tiles = int64_t((p.M + G_BM - 1) / G_BM) * ((p.N + G_BN - 1) / G_BN) * p.batch;
     int splits = 1;
-    if (tiles < c.sms && p.KT >= 4) {
+    if (tiles < c.sms && p.KT >= 4 && !p.dtrans) {  // (the transposed store has no split-K reduction)
       splits = int(std::min<int64_t>((2 * c.sms + tiles - 1) / tiles, p.KT / 2));
       const int64_t cap = PART_TILES * G_BM * G_BN / (int64_t(p.M) * p.N * p.batch);
       splits = int(std::max<int64_t>(1, std::min<int64_t>(splits, cap)));
@@ -460,9 +465,14 @@ struct Gemm {
     TcEpiMaps em;
     memset(&em, 0, sizeof(em));
     if (tc_epi_maps(em)) {
+      if (p.dtrans) {
+        if (bn == 64) return launch_tc32_k<A_, B_, 2, CD_TC_EPI_STG64, 64>(units, tm, em);
+        return launch_tc32_k<A_, B_, 2, CD_TC_EPI_STG, 128>(units, tm, em);
+      }
       if (bn == 64) return launch_tc32_k<A_, B_, 1, CD_TC_EPI_STG64, 64>(units, tm, em);
       return launch_tc32_k<A_, B_, 1, CD_TC_EPI_STG, 128>(units, tm, em);
     }
+    if (p.dtrans) return false;
     if (bn == 64) return launch_tc32_k<A_, B_, 0, TC_STAGES, 64>(units, tm, em);
     return launch_tc32_k<A_, B_, 0, TC_STAGES, 128>(units, tm, em);
   }
@@ -475,6 +485,16 @@ struct Gemm {
                          p.Cin.stride == p.D.stride;
     if (p.tril && !(has_cin && inplace)) return false;
     if (has_cin && p.Cin.arr) return false;
+    if (p.dtrans) {  // N x M views, 32 x 128 boxes with the 128-byte swizzle (gemm_tc32.cuh, EPI = 2)
+      if (p.tril) return false;
+      const float* pd = static_cast<const float*>(p.D.base) + p.D.off;
+      if (!make_tmap_f32_sw128(&em.d, pd, p.N, p.M, p.D.ld, p.D.stride, p.batch, 32, 128, false)) return false;
+      if (has_cin) {
+        const float* pc = static_cast<const float*>(p.Cin.base) + p.Cin.off;
+        if (!make_tmap_f32_sw128(&em.cin, pc, p.N, p.M, p.Cin.ld, p.Cin.stride, p.batch, 32, 128, false)) return false;
+      }
+      return true;
+    }
     const float* pd = static_cast<const float*>(p.D.base) + p.D.off;
     if (!make_tmap_f32_plain(&em.d, pd, p.M, p.N, p.D.ld, p.D.stride, p.batch, 128, 32)) return false;
     if (has_cin) {
@@ -509,6 +529,11 @@ struct Gemm {
       else if (TA == 1 && TB == 0) done = launch_tc32<1, 0>(grid);
       else done = launch_tc32<1, 1>(grid);
       if (done) return;
+    }
+    if (p.dtrans) {  // only the fp32 TMA epilogue stores transposed; the callers check first
+      c.err = CD_ERR_UNSUPPORTED;
+      snprintf(g_cuda_err, sizeof(g_cuda_err), "transposed-output GEMM needs the fp32 TMA epilogue");
+      return;
     }
     if constexpr (sizeof(T) == 8) {
       bool done = false;
@@ -657,6 +682,23 @@ static T* shared_dinv(int n, int nb) {
   return (g_ext_dinv && g_ext_dinv_nb == nb && n % nb == 0) ? static_cast<T*>(const_cast<void*>(g_ext_dinv)) : nullptr;
 }
 
+// the transposed Rbar update (blocked_rev) applies to fp32 batches whose operands the tcgen05
+// kernel's TMA maps can describe (16-byte aligned views, ld and batch stride multiples of 4)
+static bool g_no_rbar_trans = getenv("CD_NO_RBAR_TRANS") != nullptr;
+template <typename T>
+static bool rbar_transposed(const Ctx& c, int64_t batch, int q, int w, Opnd L, Opnd A, int j, Opnd W) {
+  if (sizeof(T) != 4 || batch < 2 || g_no_rbar_trans || g_tc32_disabled || g_tma_disabled || !g_tc_epi) return false;
+  if (w % 4) return false;  // S (ld = w) must be TMA-describable too
+  auto ok = [&](const Opnd& o, int64_t r0, int64_t c0) {
+    if (o.arr || o.ld % 4 || o.stride % 4) return false;
+    if (c.plan) return true;
+    const float* ptr = static_cast<const float*>(o.base) + o.off + r0 + c0 * o.ld;
+    return reinterpret_cast<uintptr_t>(ptr) % 16 == 0;
+  };
+  (void)q;
+  return ok(A, j, 0) && ok(L, j, 0) && ok(W, 0, 0);
+}
+
 template <typename T>
 static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, T* part_ws) {
   const int nblk = nblocks(n, nb);
@@ -694,7 +736,14 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
     // Dbar <- chol_unblocked_rev(D, Dbar)  (+ S = Dbar + Dbar^T)      (w <= DC_NMAX)
     run_sweep_small<T>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, q > 0 ? S : null_opnd(), nullptr);
     // Rbar <- Rbar - Cbar^T B - (Dbar + Dbar^T) R
-    if (q > 0) {
+    if (q > 0 && rbar_transposed<T>(c, batch, q, w, L, A, j, W)) {
+      // fp32 batches: as Rbar^T -= [R; B]^T [S; Cbar] -- M = q rows of 128-row tiles instead of
+      // M = w = 64 (half-empty tcgen05 tiles), the result stored transposed by the TMA epilogue
+      Gemm<T> g(c, q, w, 1, 0, batch);
+      g.seg(sub(L, j, 0), S, w);
+      if (p > 0) g.seg(sub(L, k, 0), W, p);
+      g.trans_out().run(sub(A, j, 0), sub(A, j, 0), -1.0, 1.0, 0, part_ws);
+    } else if (q > 0) {
       Gemm<T> g(c, w, q, 1, 0, batch);
       g.seg(S, sub(L, j, 0), w);
       if (p > 0) g.seg(W, sub(L, k, 0), p);

@@ -39,6 +39,7 @@ struct GemmParams {
   double alpha, beta;
   int tril;   // 0: full output; t > 0: write only rows r, cols c with r + (t - 1) >= c
   void* part; // split-K partials: [split][batch][N][M]
+  int dtrans; // 1: D and Cin hold the TRANSPOSED result (N x M, ld as given); fp32 TMA epilogue only
 };
 
 template <typename T, int TA, int TB>

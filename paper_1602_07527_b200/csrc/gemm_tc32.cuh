@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? CD_TC_EPI_MINB : CD_TC
         if (lane == 0) mbar_arrive(&conv[s]);
       }
     }
-  } else if (EPI == 1 && warp == 6) {
+  } else if (EPI >= 1 && warp == 6) {
     // ---------------- epilogue TMA warp (lane 0): Cin prefetch and output stores ----------------
     if (lane == 0) {
       const bool has_cin = p.beta != 0.0;
@@ -347,8 +347,10 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? CD_TC_EPI_MINB : CD_TC
         const int slot = lg % TC_ESLOTS;
         if (has_cin) {
           mbar_expect_tx(&cinf[slot], TC_ECHUNK_BYTES);
-          if (tm.batched) tma_load_3d(Es + slot * TC_ECHUNK_BYTES, &em.cin, m0, n0 + 32 * lc, int(b), &cinf[slot]);
-          else tma_load_2d(Es + slot * TC_ECHUNK_BYTES, &em.cin, m0, n0 + 32 * lc, &cinf[slot]);
+          // EPI = 2: D (and Cin) are stored transposed, so the chunk is a 32-row x 128-column box
+          const int x0 = EPI == 2 ? n0 + 32 * lc : m0, x1 = EPI == 2 ? m0 : n0 + 32 * lc;
+          if (tm.batched) tma_load_3d(Es + slot * TC_ECHUNK_BYTES, &em.cin, x0, x1, int(b), &cinf[slot]);
+          else tma_load_2d(Es + slot * TC_ECHUNK_BYTES, &em.cin, x0, x1, &cinf[slot]);
         } else {
           mbar_arrive(&cinf[slot]);
         }
@@ -366,8 +368,9 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? CD_TC_EPI_MINB : CD_TC
           const int slot = g % TC_ESLOTS;
           tc_wait(&donef[slot], (g / TC_ESLOTS) & 1);
           unsigned char* E = Es + slot * TC_ECHUNK_BYTES;
-          if (tm.batched) tma_store_3d(&em.d, E, m0, n0 + 32 * c, int(b));
-          else tma_store_2d(&em.d, E, m0, n0 + 32 * c);
+          const int x0 = EPI == 2 ? n0 + 32 * c : m0, x1 = EPI == 2 ? m0 : n0 + 32 * c;
+          if (tm.batched) tma_store_3d(&em.d, E, x0, x1, int(b));
+          else tma_store_2d(&em.d, E, x0, x1);
           asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
           // chunk g + ESLOTS - 1 takes the slot of chunk g - 1 once that store has read it
           asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? CD_TC_EPI_MINB : CD_TC
       }
       asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
-  } else if (EPI == 1) {
+  } else if (EPI >= 1) {
     // ---------------- TMA epilogue: warps 2..5, thread = accumulator row ----------------
     const int q = warp & 3;
     const int rr = q * 32 + lane;  // row within the tile (TMEM lane)
@@ -415,13 +418,29 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? CD_TC_EPI_MINB : CD_TC
           if (lane == 0) mbar_arrive(&acce[buf]);
         }
         tc_wait(&cinf[slot], (g / TC_ESLOTS) & 1);  // Cin landed / slot released
+        if constexpr (EPI == 2) {
+          // transposed chunk: row rr of the box holds this thread's 32 values (128 B), its
+          // 16-byte pieces permuted by the 128-byte swizzle (piece ^ (rr & 7)): conflict-free
+          float4* E4 = reinterpret_cast<float4*>(E) + rr * 8;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const int col = n0 + 32 * c + jj;
-          const float acc = nkt > 0 ? __uint_as_float(v[jj]) : 0.f;
-          const float ci = has_cin ? E[jj * 128 + rr] : 0.f;
-          const bool keep = p.tril && !(r + p.tril - 1 >= col);
-          E[jj * 128 + rr] = keep ? ci : alpha * acc + beta * ci;
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const int ch = q4 ^ (rr & 7);
+            const float4 ci = has_cin ? E4[ch] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float a[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) a[e] = nkt > 0 ? __uint_as_float(v[4 * q4 + e]) : 0.f;
+            E4[ch] = make_float4(alpha * a[0] + beta * ci.x, alpha * a[1] + beta * ci.y, alpha * a[2] + beta * ci.z,
+                                 alpha * a[3] + beta * ci.w);
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int col = n0 + 32 * c + jj;
+            const float acc = nkt > 0 ? __uint_as_float(v[jj]) : 0.f;
+            const float ci = has_cin ? E[jj * 128 + rr] : 0.f;
+            const bool keep = p.tril && !(r + p.tril - 1 >= col);
+            E[jj * 128 + rr] = keep ? ci : alpha * acc + beta * ci;
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
