@@ -860,6 +860,10 @@ static int64_t g_ll_pieces = getenv("CD_LL_PIECES") ? atoi(getenv("CD_LL_PIECES"
 // the SYMM moves into the panel kernel while its 32 x 32 output tiles number <= this x #SMs
 static int64_t g_symm_in_panel = getenv("CD_SYMM_IN_PANEL") ? atoi(getenv("CD_SYMM_IN_PANEL")) : 1;
 static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DEBUG_PANEL_SKIP")) : 0;
+// k_fwd_sk CTAs: at most ~PIECES pieces per output tile (0 = no cap); the cap only binds on the last
+// ~10 panels of a sweep (m < 10 tiles), where the last arriver otherwise sums up to ~30 partial tiles
+// (N = 4096: 5.53 -> 5.24 ms with 16; N = 1024 and 16384 unchanged; 4 and 8 were slower)
+static int64_t g_fs_pieces = getenv("CD_FS_PIECES") ? atoi(getenv("CD_FS_PIECES")) : 16;
 static bool g_no_bal1 = getenv("CD_NO_BAL1") != nullptr;  // forward panel: one CTA per 128-wide K chunk
 
 static int panel_occupancy() {
@@ -1231,6 +1235,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
         return;
       }
       fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
+      if (g_fs_pieces > 0) fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, g_fs_pieces * batch * fp.m)));
       fp.part = skpart;
       fp.cnt = cnt;
       fp.chol = 0;
