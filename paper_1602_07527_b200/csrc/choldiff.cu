@@ -1321,6 +1321,8 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
       return;
     }
     fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
+    if (g_fs_pieces > 0)  // (fused sweep N = 4096: 12.54 -> 12.12 ms)
+      fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, g_fs_pieces * batch * fp.m)));
     fp.part = skpart;
     fp.cnt = cnt;
     fp.chol = chol;
