@@ -280,7 +280,8 @@ def test_f32_left_looking_nan_upper(n):
     assert nerr(out, oracle.chol_rev(L, Lb)) < 2.5e-5
 
 
-@pytest.mark.parametrize("n,B,dt", [(300, 3, torch.float64), (512, 2, torch.float32), (40, 5, torch.float64)])
+@pytest.mark.parametrize("n,B,dt", [(300, 3, torch.float64), (512, 2, torch.float32), (40, 5, torch.float64),
+                                    (1100, 1, torch.float32), (700, 1, torch.float64)])
 def test_rev_fwd_two_streams_equal_separate_calls(n, B, dt):
     L, Lb, Sd = synthetic.draw_batch(n, B, seed=8 * n, sdot=True)
     Lt, Lbt, St = to_dev(L, dt), to_dev(Lb, dt), to_dev(np.tril(Sd), dt)
