@@ -1,13 +1,14 @@
 // gemm_tc32.cuh -- fp32 Level-3 updates of the blocked sweeps (PAPER.md:634-636, 655-666,
 // 689-701) on the 5th-generation tensor cores: tcgen05.mma kind::tf32 with the
-// accumulator in TMEM, operands staged by TMA (128-byte swizzle) into a 4-stage ring.
+// accumulator in TMEM, operands staged by TMA (128-byte swizzle) into a 4- or 5-stage ring.
 //
 //   warp 0 lane 0 : TMA producer (cp.async.bulk.tensor, mbarrier complete_tx)
 //   warp 1 lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128 N=128 K=8;
 //                   tcgen05.commit releases each smem stage and finally the accumulator)
 //   warps 2..5    : epilogue (tcgen05.ld 32x32b: thread = accumulator row)
-//   warp 6        : (EPI = 1) the epilogue's TMA warp: prefetches Cin chunks into smem slots
-//                   and stores finished chunks with cp.async.bulk.tensor
+//   warp 6        : (EPI >= 1) the epilogue's TMA warp: prefetches Cin chunks into smem slots
+//                   and stores finished chunks with cp.async.bulk.tensor (EPI = 2: transposed,
+//                   through 32 x 128 boxes with the 128-byte swizzle)
 //   last 8 warps  : round each landed operand stage to tf32 in place (cvt.rna) -- SURVEY c11:
 //                   the MMA would otherwise truncate the low 13 mantissa bits (biased error;
 //                   rounding cut the batched N = 512 error 4.3e-5 -> 1.1e-5 against the 1e-4 gate)
