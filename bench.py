@@ -21,6 +21,15 @@ The same JSON line carries, measured in the same run:
 --impl reference: the CPU oracle (the reference arm for this tier) timed on the
 same metric / config, each step a bounded sample (the trailing columns of the
 sweep), rank 0 only.
+
+Multi-GPU: ``python bench.py --gpus N`` (N > 1) started without a torchrun environment
+re-executes itself under ``torch.distributed.run`` with N ranks (one per GPU, NCCL,
+rendezvous on 127.0.0.1), and every rank checks WORLD_SIZE == --gpus.  The batched
+configs shard by matrix; their compute is timed as the max over ranks and the NCCL
+gather of the results is timed separately ("gather").  NCCL_DEBUG=INFO is set for
+the ranks, its output written to nccl_logs/ (the JSON line stays the only stdout).
+``--dry-run`` runs the same rank/shard/gather plumbing on the CPU with gloo (no GPU,
+no kernels, no timing numbers): ``python bench.py --gpus 2 --dry-run``.
 """
 from __future__ import annotations
 
@@ -41,6 +50,15 @@ METRIC = "chol_rev GFLOP/s (fp64, N=16384) and batched matrices/s; % of roofline
 FP64_PEAK_TFLOPS = 37.0     # measured DMMA issue-rate peak (tools/microbench_fp64.cu, profiles/r01_microbench_fp64.txt)
 CUBLAS_DGEMM_TFLOPS = 35.5  # measured torch.matmul fp64 8192^3 (profiles/r01_torch_peaks.json), context only
 TF32_PEAK_TFLOPS = 1638.4 / 2  # MEASURED_PEAKS bf16 dense x the guide's nominal tf32:bf16 ratio (1:2)
+
+
+def _generator_version():
+    sys.path.insert(0, ROOT)
+    import synthetic
+    return synthetic.GENERATOR_VERSION
+
+
+GEN = _generator_version()
 
 
 def rev_flops(n: int) -> int:
@@ -120,43 +138,77 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- distributed
 class Dist:
-    def __init__(self, want: int):
+    """One process per GPU (torchrun environment).  NCCL on the GPUs; gloo on the CPU for
+    --dry-run.  Fails loudly when the launched world size is not the requested --gpus."""
+
+    def __init__(self, want: int, dry_run: bool = False):
         import torch
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.want = want
+        self.dry = dry_run
+        if self.world != want:
+            raise SystemExit(f"bench.py: --gpus {want} but the launch has WORLD_SIZE={self.world} "
+                             "(start it as `python bench.py --gpus N`, or under torchrun with N ranks)")
         self.pg = None
+        self.device = torch.device("cpu") if dry_run else torch.device("cuda", self.local)
         if self.world > 1:
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if dry_run:
+                dist.init_process_group("gloo")
+            else:
+                nccl_env()
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
-        self.device = torch.device("cuda", self.local)
+        self.backend = (self.pg.get_backend() if self.pg else None)
 
     def barrier(self):
         if self.pg:
             self.pg.barrier()
 
-    def max(self, x: float) -> float:
-        if not self.pg:
-            return x
+    def _reduce(self, x: float, op) -> float:
         import torch
         t = torch.tensor([x], dtype=torch.float64, device=self.device)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        self.pg.all_reduce(t, op=op)
         return float(t.item())
 
+    def max(self, x: float) -> float:
+        return self._reduce(x, self.pg.ReduceOp.MAX) if self.pg else x
+
     def sum(self, x: float) -> float:
-        if not self.pg:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64, device=self.device)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
-        return float(t.item())
+        return self._reduce(x, self.pg.ReduceOp.SUM) if self.pg else x
 
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
+
+
+NCCL_LOG_DIR = os.path.join(ROOT, "nccl_logs")
+
+
+def nccl_env():
+    """NCCL_DEBUG=INFO for the ranks (communicator setup and ranks visible), written to
+    nccl_logs/ so that stdout carries only the JSON line."""
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    if "NCCL_DEBUG_FILE" not in os.environ:
+        os.makedirs(NCCL_LOG_DIR, exist_ok=True)
+        os.environ["NCCL_DEBUG_FILE"] = os.path.join(NCCL_LOG_DIR, "nccl.%h.%p.log")
+
+
+def relaunch_under_torchrun(nranks: int) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: start N ranks of this very
+    command under torch.distributed.run (127.0.0.1 rendezvous) and return their exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    nccl_env()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=dict(os.environ))
 
 
 # ----------------------------------------------------------------------------- timing
@@ -206,10 +258,11 @@ def bench_single_rev(args, dist: Dist):
 
     n, nb = args.n, args.nb
     t0 = time.time()
-    L, Lb, _ = synthetic.draw(n, args.seed)
+    L, Lb, Sd = synthetic.draw(n, args.seed, sdot=args.fwd_steps > 0 or args.fused_steps > 0)
     Lcm = synthetic.to_colmajor(L)
     Acm = synthetic.to_colmajor(Lb)
-    del L, Lb
+    Fcm = synthetic.to_colmajor(np.tril(Sd)) if Sd is not None else None
+    del L, Lb, Sd
     gen_s = time.time() - t0
     dev = dist.device
     Ld = torch.from_numpy(Lcm).to(dev).transpose(0, 1)
@@ -259,7 +312,11 @@ def bench_single_rev(args, dist: Dist):
                     "max": round(max(ms), 3)},
         "gpu_launches": int(launches),
         "input_generation_s": round(gen_s, 1),
+        "generator": GEN,
     }
+    if dist.world > 1:
+        out["nccl"] = {"backend": dist.backend, "world_size": dist.world,
+                       "debug": os.environ.get("NCCL_DEBUG"), "debug_file": os.environ.get("NCCL_DEBUG_FILE")}
     total_ms = sum(v[0] for v in prof.values())
     # dominant kernel class = the largest device-time share among the tensor-core classes
     dom = max(("symm", "gemm", "panel"), key=lambda k: prof[k][0])
@@ -285,18 +342,24 @@ def bench_single_rev(args, dist: Dist):
             out["roofline"]["hbm_peak_gbs"] = peaks.get("hbm_gbs")
     out["clocks"] = clk.summary()
 
-    # ---- the blocked forward sweep alongside, same N and L; Sigma_dot's
-    # lower triangle is an N(0,1) draw like L_bar's, so tril(L_bar) serves as its input
+    # ---- the blocked forward sweep alongside, same N and L, the generator's
+    # Sigma_dot (its 4th draw, synthetic/)
     if args.fwd_steps > 0:
+        F0 = torch.from_numpy(Fcm).to(dev).transpose(0, 1)
+
         def fstep():
             cd.chol_fwd(Ld, A, nb=nb)
 
-        fms = timed_steps(fstep, restore, args.fwd_steps, 1, dist, stream)
+        def frestore():
+            A.copy_(F0)
+
+        fms = timed_steps(fstep, frestore, args.fwd_steps, 1, dist, stream)
         fw = dist.max(statistics.mean(fms))
         out["fwd"] = {"workload": f"chol_fwd fp64 single matrix N={n} (same L), nb={nb}",
                       "ms_per_step": round(fw, 3), "value": round(fwd_flops(n) / (fw * 1e-3) / 1e9, 2),
                       "unit": "GFLOP/s", "frac_of_fp64_peak": round(fwd_flops(n) / (fw * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                       "steps": args.fwd_steps}
+        del F0
 
     # ---- factorisation + forward mode fused in one sweep (Sigma = L L^T as input)
     if args.fused_steps > 0:
@@ -306,9 +369,11 @@ def bench_single_rev(args, dist: Dist):
         def ustep():
             cd.chol_fwd_fused(Sw, A)
 
+        F0 = torch.from_numpy(Fcm).to(dev).transpose(0, 1)
+
         def urestore():
             Sw.copy_(S0)
-            A.copy_(A0)
+            A.copy_(F0)
 
         ums = timed_steps(ustep, urestore, args.fused_steps, 1, dist, stream)
         uw = dist.max(statistics.mean(ums))
@@ -316,7 +381,7 @@ def bench_single_rev(args, dist: Dist):
         out["chol_fwd_fused"] = {"workload": f"cd_chol_fwd_fused fp64 N={n}: Sigma -> L and Sigma_dot -> L_dot in one sweep",
                                  "ms_per_step": round(uw, 3), "value": round(ufl / (uw * 1e-3) / 1e9, 2),
                                  "unit": "GFLOP/s (N^3/3 factorisation + fwd(N))", "steps": args.fused_steps}
-        del S0, Sw
+        del S0, Sw, F0
 
     # ---- e2e through the host-buffer C-ABI call
     if args.e2e_steps > 0:
@@ -458,7 +523,8 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
                         "peak": hbm, "unit": "GB/s", "frac": round(achieved_gbs / hbm, 4),
                         "algorithmic_bytes_per_matrix": algo_bytes,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs", "traffic": load_traffic("bulk32")},
-           "gpu_launches": int(launches), "clocks": clk.summary()}
+           "gpu_launches": int(launches), "clocks": clk.summary(), "generator": GEN,
+           "l2": "inputs larger than L2 (512 MiB per array)"}
     # the symbolic route (Eq. 10 on the whole matrix, north star (d)) on the same inputs, for
     # the route choice "by measurement" (AUTO = algorithmic)
     sms = timed_steps(lambda: cd.chol_rev(Ld, A, route="symbolic"), restore, 5, 2, dist, stream)
@@ -466,20 +532,7 @@ def bench_batched(args, dist: Dist, n=32, total=65536, seed=0, gather=True):
                              "matrices_per_s": round(total / (dist.max(statistics.mean(sms)) * 1e-3), 1),
                              "kernel": "k_symbolic_cta (one CTA per matrix, Eq. 10 on 8x8 DMMA tiles)"}
     if gather and P > 1:
-        # NCCL used only to gather the sharded results (north star), timed separately
-        torch.cuda.synchronize()
-        dist.barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        gathered = gather_batches(A, total)
-        b.record(stream)
-        torch.cuda.synchronize()
-        g = dist.max(a.elapsed_time(b))
-        del gathered
-        out["gather"] = {"ms": round(g, 3), "bytes": total * n * n * 8,
-                         "GBps": round(total * n * n * 8 / (g * 1e-3) / 1e9, 1),
-                         "collective": "all_gather_into_tensor (paper_1602_07527_b200/shard.py)"}
+        out["gather"] = timed_gather(dist, stream, [A], total)
     if dist.world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_sample_batched(L, Lb, n)
     return out
@@ -501,84 +554,211 @@ def cpu_sample_batched(L, Lb, n, sample=16384):
             "sample": f"first {s} of the 65536 N={n} matrices, oracle/oracle.c or_chol_rev_batched (OpenMP over matrices)"}
 
 
+class L2Flush:
+    """Writes a buffer larger than the 126 MB L2 (outside the timed events) so that every
+    timed iteration of a small configuration starts from a cold L2 (timing rules)."""
+
+    def __init__(self, device, nbytes=256 << 20):
+        import torch
+        self.buf = torch.empty(nbytes // 4, dtype=torch.float32, device=device)
+        self.k = 0
+
+    def __call__(self):
+        self.k += 1
+        self.buf.fill_(float(self.k))
+
+
+def cpu_oracle_single(kind: str, L, X, reps_seconds=2.0):
+    """Oracle (plain C, ONE thread) on one matrix, repeated for about `reps_seconds`:
+    kind 'rev' or 'fwd'.  Returns seconds per call."""
+    import oracle
+    n = L.shape[0]
+    Lc = synthetic_cm(L)
+    X0 = synthetic_cm(X)
+    f = oracle.chol_rev_colmajor_inplace if kind == "rev" else oracle.chol_fwd_serial_colmajor_inplace
+    oracle.set_threads(1)
+    try:
+        reps, t_tot = 0, 0.0
+        while t_tot < reps_seconds or reps < 3:
+            A = X0.copy()
+            t0 = time.perf_counter()
+            f(n, Lc, A)
+            t_tot += time.perf_counter() - t0
+            reps += 1
+    finally:
+        oracle.set_threads(0)
+    return t_tot / reps, reps
+
+
+def synthetic_cm(m):
+    import synthetic
+    return synthetic.to_colmajor(m).copy()
+
+
 def bench_small_configs(args, dist: Dist):
     """configs[0] (N=64 rev latency), configs[1] (N=1024 rev + fwd) and configs[3]
-    (1024 x N=512 fp32 rev + fwd, sharded by matrix), same timing rules."""
+    (1024 x N=512 fp32 rev + fwd, sharded by matrix), same timing rules; each with the
+    oracle timed beside it on the host cores (rank 0 at N=1)."""
     import torch
     import paper_1602_07527_b200 as cd
     import synthetic
 
     dev = dist.device
     stream = torch.cuda.current_stream(dev)
+    flush = L2Flush(dev)
+    cpu = dist.world == 1 and not args.no_cpu
     out = {}
-    # configs[0]: single fp64 N=64 reverse (latency)
+    # configs[0]: single fp64 N=64 reverse (latency); L2 flushed before every timed call
     L, Lb, _ = synthetic.draw(64, 0)
     Ld, A0 = colmajor_dev(L, dev), colmajor_dev(Lb, dev)
     A = A0.clone()
-    ms = timed_steps(lambda: cd.chol_rev(Ld, A), lambda: A.copy_(A0), 50, args.warmup, dist, stream)
+
+    def r0():
+        A.copy_(A0)
+        flush()
+
+    ms = timed_steps(lambda: cd.chol_rev(Ld, A), r0, 50, args.warmup, dist, stream)
     t = dist.max(statistics.median(ms))
     # the same call captured once in a CUDA graph and replayed (host launch overhead removed)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         cd.chol_rev(Ld, A)
-    gms = timed_steps(g.replay, lambda: A.copy_(A0), 50, args.warmup, dist, stream)
+    gms = timed_steps(g.replay, r0, 50, args.warmup, dist, stream)
     tg = dist.max(statistics.median(gms))
     out["n64_rev"] = {"workload": "configs[0]: chol_rev fp64 N=64, seed 0", "us_per_call": round(t * 1e3, 2),
                       "gflops": round(rev_flops(64) / (t * 1e-3) / 1e9, 2),
-                      "us_per_call_cuda_graph": round(tg * 1e3, 2)}
+                      "us_per_call_cuda_graph": round(tg * 1e3, 2), "l2": "flushed before every timed call",
+                      "generator": GEN}
+    if cpu:
+        sec, reps = cpu_oracle_single("rev", L, Lb)
+        out["n64_rev"]["cpu_baseline"] = {"value": round(sec * 1e6, 2), "unit": "us per call", "cores": 1,
+                                          "threads": 1, "kind": "oracle",
+                                          "sample": f"the whole N=64 reverse sweep, {reps} calls, "
+                                                    "oracle/oracle.c or_chol_rev_partial (single thread)"}
     # configs[1]: N=1024 reverse and forward
     L, Lb, Sd = synthetic.draw(1024, 0, sdot=True)
     Ld, A0, F0 = colmajor_dev(L, dev), colmajor_dev(Lb, dev), colmajor_dev(np.tril(Sd), dev)
     A, F = A0.clone(), F0.clone()
-    tr = dist.max(statistics.median(timed_steps(lambda: cd.chol_rev(Ld, A), lambda: A.copy_(A0), 10, args.warmup,
-                                                dist, stream)))
-    tf = dist.max(statistics.median(timed_steps(lambda: cd.chol_fwd(Ld, F), lambda: F.copy_(F0), 10, args.warmup,
-                                                dist, stream)))
-    ts = dist.max(statistics.median(timed_steps(lambda: cd.chol_rev(Ld, A, route="symbolic"), lambda: A.copy_(A0),
+
+    def ra():
+        A.copy_(A0)
+        flush()
+
+    def rf():
+        F.copy_(F0)
+        flush()
+
+    tr = dist.max(statistics.median(timed_steps(lambda: cd.chol_rev(Ld, A), ra, 10, args.warmup, dist, stream)))
+    tf = dist.max(statistics.median(timed_steps(lambda: cd.chol_fwd(Ld, F), rf, 10, args.warmup, dist, stream)))
+    ts = dist.max(statistics.median(timed_steps(lambda: cd.chol_rev(Ld, A, route="symbolic"), ra,
                                                 5, args.warmup, dist, stream)))
     out["n1024"] = {"workload": "configs[1]: fp64 N=1024, seed 0", "rev_ms": round(tr, 3), "fwd_ms": round(tf, 3),
                     "rev_symbolic_route_ms": round(ts, 3),
                     "rev_gflops": round(rev_flops(1024) / (tr * 1e-3) / 1e9, 1),
-                    "fwd_gflops": round(fwd_flops(1024) / (tf * 1e-3) / 1e9, 1)}
+                    "fwd_gflops": round(fwd_flops(1024) / (tf * 1e-3) / 1e9, 1),
+                    "rev_frac_of_fp64_peak": round(rev_flops(1024) / (tr * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                    "fwd_frac_of_fp64_peak": round(fwd_flops(1024) / (tf * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                    "l2": "flushed before every timed call", "generator": GEN}
+    if cpu:
+        sr, nr = cpu_oracle_single("rev", L, Lb)
+        sf, nf = cpu_oracle_single("fwd", L, np.tril(Sd))
+        out["n1024"]["cpu_baseline"] = {
+            "value": round((rev_flops(1024) + fwd_flops(1024)) / (sr + sf) / 1e9, 3), "unit": "GFLOP/s",
+            "rev_ms": round(sr * 1e3, 1), "fwd_ms": round(sf * 1e3, 1), "cores": 1, "threads": 1, "kind": "oracle",
+            "sample": f"the whole N=1024 reverse ({nr} calls) and forward ({nf} calls) sweeps, oracle/oracle.c "
+                      "(single thread)"}
     # configs[3]: 1024 x N=512 fp32, reverse + forward per step, sharded by matrix
     n, total = 512, 1024
-    from paper_1602_07527_b200.shard import shard_range
+    from paper_1602_07527_b200.shard import gather_batches, shard_range
     P, r = dist.world, dist.rank
     lo, hi = shard_range(total, P, r)
     L, Lb, Sd = synthetic.draw_batch(n, hi - lo, seed=0, sdot=True, start=lo)
     Ld = colmajor_dev(L, dev, torch.float32)
     A0 = colmajor_dev(Lb, dev, torch.float32)
     F0 = colmajor_dev(np.tril(Sd), dev, torch.float32)
-    del L, Lb, Sd
     A, F = A0.clone(), F0.clone()
 
-    def step():  # both sweeps of the same factors; chol_rev_fwd runs them on two streams
+    def step():  # both sweeps of the same factors in one library call
         cd.chol_rev_fwd(Ld, A, F)
 
     def restore():
         A.copy_(A0)
         F.copy_(F0)
 
-    t = dist.max(statistics.median(timed_steps(step, restore, 5, args.warmup, dist, stream)))
+    with ClockSampler(dev) as clk:
+        ms3 = timed_steps(step, restore, args.steps_c3, args.warmup, dist, stream,
+                          before_timed=cd.reset_launch_count)
+    launches = cd.launch_count()
+    t = dist.max(statistics.median(ms3))
     fl = (rev_flops(n) + fwd_flops(n)) * total
+    algo = 5 * (n * (n + 1) // 2) * 4
+    hbm = measured_peaks().get("hbm_gbs", 6536.0)
+    achieved = algo * total / P / (t * 1e-3) / 1e9  # per GPU
     out["batched_f32_n512"] = {
         "workload": f"configs[3]: fp32 rev + fwd, {total} x N={n}, sharded by matrix over {P} GPU(s); "
-                    "cd.chol_rev_fwd (the two independent sweeps on two streams)",
+                    "cd.chol_rev_fwd (cd_chol_rev_fwd_strided_batched)",
         "ms_per_step": round(t, 3), "matrices_per_s": round(total / (t * 1e-3), 1),
-        "gflops": round(fl / (t * 1e-3) / 1e9, 1),
-        # engines: tcgen05 kind::tf32 GEMMs + fp64-DMMA on-chip diagonal blocks.  Roofline =
-        # max(bytes / HBM, flops / tf32 peak); the HBM term wins: 5 T(512) fp32 triangles per
-        # matrix moved once (L shared by rev and fwd; SURVEY 8d), 0.41 ms for the batch
-        "roofline": {"bound": "hbm", "unit": "GB/s",
-                     "algorithmic_bytes_per_matrix": 5 * (n * (n + 1) // 2) * 4,
-                     "achieved": round(5 * (n * (n + 1) // 2) * 4 * total / P / (t * 1e-3) / 1e9, 1),
-                     "peak": measured_peaks().get("hbm_gbs", 6536.0),
-                     "frac": round(5 * (n * (n + 1) // 2) * 4 * total / P / (t * 1e-3) / 1e9
-                                   / measured_peaks().get("hbm_gbs", 6536.0), 4),
+        "gflops": round(fl / (t * 1e-3) / 1e9, 1), "steps": args.steps_c3,
+        "step_ms": {"min": round(min(ms3), 3), "median": round(statistics.median(ms3), 3),
+                    "max": round(max(ms3), 3)},
+        "gpu_launches": int(launches) // max(1, args.steps_c3), "clocks": clk.summary(), "generator": GEN,
+        "l2": "inputs larger than L2 (1 GiB per array)",
+        # roofline = max(bytes / HBM, flops / tf32 peak); the HBM term wins: 5 T(512) fp32
+        # triangles per matrix moved once (L shared by rev and fwd; SURVEY 8d), 0.41 ms for the batch
+        "roofline": {"bound": "hbm", "unit": "GB/s", "algorithmic_bytes_per_matrix": algo,
+                     "achieved": round(achieved, 1), "peak": hbm, "frac": round(achieved / hbm, 4),
                      "compute_floor_ms": round(fl / P / TF32_PEAK_TFLOPS / 1e9, 3),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs; tf32 peak = measured bf16 dense x 1/2 "
                                     "(profiling guide's nominal ratio)"}}
+    if P > 1:
+        out["batched_f32_n512"]["gather"] = timed_gather(dist, stream, [A, F], total)
+    if cpu:
+        out["batched_f32_n512"]["cpu_baseline"] = cpu_sample_c3(L, Lb, Sd, n)
     return out
+
+
+def timed_gather(dist: Dist, stream, shards, total: int):
+    """NCCL all_gather of the per-rank result shards (north star: NCCL only to gather),
+    timed on the device as the max over ranks, outside the compute timing."""
+    import torch
+    from paper_1602_07527_b200.shard import gather_batches
+    torch.cuda.synchronize()
+    dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    outs = [gather_batches(x, total) for x in shards]
+    b.record(stream)
+    torch.cuda.synchronize()
+    g = dist.max(a.elapsed_time(b))
+    nbytes = sum(o.numel() * o.element_size() for o in outs)
+    del outs
+    return {"ms": round(g, 3), "bytes": nbytes, "GBps": round(nbytes / (g * 1e-3) / 1e9, 1),
+            "collective": "all_gather_into_tensor over NCCL (paper_1602_07527_b200/shard.py)",
+            "timed": "device events around the gathers, max over ranks, separate from compute"}
+
+
+def cpu_sample_c3(L, Lb, Sd, n, sample=48):
+    """configs[3] oracle beside the GPU: the first `sample` matrices of the batch, reverse and
+    forward, fp64 on the fp32-rounded inputs, OpenMP over matrices on all cores."""
+    ncores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(ncores))
+    import oracle
+    import synthetic
+    s = min(sample, L.shape[0])
+    r32 = lambda x: x[:s].astype(np.float32).astype(np.float64)  # noqa: E731
+    Lc = synthetic.to_colmajor(r32(L))
+    Ac = synthetic.to_colmajor(r32(Lb))
+    Fc = synthetic.to_colmajor(np.tril(r32(Sd)))
+    t0 = time.perf_counter()
+    oracle.chol_rev_batched_colmajor(n, s, Lc, Ac)
+    oracle.chol_fwd_cols_batched_colmajor(n, s, Lc, Fc)
+    dt = time.perf_counter() - t0
+    return {"value": round(s / dt, 2), "unit": "matrices/s (rev + fwd)", "cores": ncores,
+            "threads": int(os.environ.get("OMP_NUM_THREADS", ncores)), "kind": "oracle",
+            "gflops": round(s * (rev_flops(n) + fwd_flops(n)) / dt / 1e9, 3),
+            "sample": f"first {s} of the 1024 N={n} matrices, reverse + forward in fp64 on the fp32-rounded "
+                      "inputs, oracle/oracle.c (OpenMP over matrices)"}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -647,15 +827,31 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batched", action="store_true")
     ap.add_argument("--no-aux", action="store_true", help="skip configs[0], [1], [3] sub-measurements")
+    ap.add_argument("--steps-c3", type=int, default=10, help="timed steps of configs[3] (1024 x N=512 fp32)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: exercise the rank / shard / gather plumbing with gloo (no kernels, no timings)")
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
+    if args.warmup < 3 and args.impl == "ours" and not args.dry_run:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-run this command as N torchrun ranks
+        raise SystemExit(relaunch_under_torchrun(args.gpus))
 
     if args.impl == "reference":
         res = reference_arm(args)
         if res is not None:
             print(json.dumps(res), flush=True)
+        return
+
+    if args.dry_run:
+        dist = Dist(args.gpus, dry_run=True)
+        res = dry_run(args, dist)
+        if dist.rank == 0:
+            print(json.dumps(res), flush=True)
+        dist.close()
         return
 
     import torch
@@ -673,6 +869,42 @@ def main():
     if dist.rank == 0:
         print(json.dumps(res), flush=True)
     dist.close()
+
+
+def dry_run(args, dist: Dist):
+    """The multi-rank plumbing of the batched configs without a GPU: every rank takes its
+    shard_range of configs[2] / configs[3] (reduced totals), draws its own inputs (seed + index),
+    passes them through unchanged in place of the kernel, and the shards are all-gathered over
+    gloo (the same gather_batches the GPU run uses over NCCL); rank 0 checks the gathered batch
+    equals a single-process draw (partition order).  No kernel runs and nothing is timed as a
+    throughput: "value" is null."""
+    import torch
+    import synthetic
+    from paper_1602_07527_b200.shard import gather_batches, shard_range
+    P, r = dist.world, dist.rank
+    out = {"metric": METRIC, "value": None, "unit": "GFLOP/s", "n_gpus": P, "dry_run": True,
+           "backend": dist.backend, "steps": 0, "warmup": 0, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64 generator, synthetic/)",
+           "generator": GEN, "config": {"workload": "dry run: shard + gather plumbing of configs[2] / configs[3]",
+                                        "parallelism": f"by matrix over {P} ranks"}}
+    for name, n, total in (("batched", 32, 96), ("batched_f32_n512", 16, 24)):
+        lo, hi = shard_range(total, P, r)
+        _, Lb, _ = synthetic.draw_batch(n, hi - lo, seed=0, start=lo)
+        local = torch.from_numpy(synthetic.to_colmajor(Lb)).transpose(-1, -2)  # column-major per matrix
+        dist.barrier()
+        t0 = time.perf_counter()
+        g = gather_batches(local, total)
+        dt = time.perf_counter() - t0
+        gmax = dist.max(dt)
+        ok = True
+        if r == 0:
+            _, ref, _ = synthetic.draw_batch(n, total, seed=0)
+            ok = bool(np.array_equal(g.numpy(), ref))
+        out[name] = {"shards": [list(shard_range(total, P, q)) for q in range(P)], "total": total, "n": n,
+                     "gather": {"ms": round(gmax * 1e3, 3), "bytes": int(g.numel() * g.element_size()),
+                                "collective": f"all_gather over {dist.backend} (paper_1602_07527_b200/shard.py)",
+                                "order_ok": ok}}
+    return out
 
 
 if __name__ == "__main__":

@@ -59,6 +59,8 @@ def lib():
             i64, pd, pi = ctypes.c_int64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
             for name, args in {
                 "or_chol_unblocked": [i64, pd, i64],
+                "or_chol_unblocked_cols": [i64, pd, i64],
+                "or_chol_fwd_cols": [i64, pd, i64, pd, i64],
                 "or_chol_unblocked_complex": [i64, ctypes.c_void_p, i64],
                 "or_chol_fwd": [i64, pd, i64, pd, i64],
                 "or_chol_rev": [i64, pd, i64, pd, i64],
@@ -70,7 +72,9 @@ def lib():
                 f = getattr(L, name)
                 f.argtypes = args
                 f.restype = ctypes.c_int
-            for name in ("or_chol_rev_batched", "or_chol_fwd_batched"):
+            L.or_set_threads.argtypes = [ctypes.c_int]
+            L.or_set_threads.restype = None
+            for name in ("or_chol_rev_batched", "or_chol_fwd_batched", "or_chol_fwd_cols_batched"):
                 f = getattr(L, name)
                 f.argtypes = [i64, i64, pd, i64, i64, pd, i64, i64, pi]
                 f.restype = None
@@ -162,6 +166,37 @@ def chol_fwd_batched_colmajor(n, batch, L_cm, Ad_cm):
     lib().or_chol_fwd_batched(n, batch, _p(L_cm), max(1, n), n * n, _p(Ad_cm), max(1, n), n * n,
                               info.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
     return info
+
+
+def chol_fwd_cols_batched_colmajor(n, batch, L_cm, Ad_cm):
+    """As chol_fwd_batched_colmajor, column-ordered evaluation (bit-identical, faster at large n)."""
+    info = np.zeros(batch, dtype=np.int32)
+    lib().or_chol_fwd_cols_batched(n, batch, _p(L_cm), max(1, n), n * n, _p(Ad_cm), max(1, n), n * n,
+                                   info.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    return info
+
+
+def chol_fwd_colmajor_inplace(n, L_cm, Ad_cm):
+    """In-place forward sweep on column-major buffers (C-contiguous arrays
+    whose bytes are column-major), column-ordered evaluation, OpenMP over rows: bit-identical
+    to chol_fwd (tests/test_oracle.py), for the full-size parity tests.  Returns the info code."""
+    return lib().or_chol_fwd_cols(n, _p(L_cm), max(1, n), _p(Ad_cm), max(1, n))
+
+
+def chol_fwd_serial_colmajor_inplace(n, L_cm, Ad_cm):
+    """The plain row-wise forward sweep (or_chol_fwd, no OpenMP) on column-major buffers."""
+    return lib().or_chol_fwd(n, _p(L_cm), max(1, n), _p(Ad_cm), max(1, n))
+
+
+def set_threads(t: int) -> None:
+    """OpenMP threads of the oracle's parallel loops (0 = all cores).  Scheduling only."""
+    lib().or_set_threads(int(t))
+
+
+def chol_colmajor_inplace(n, A_cm):
+    """In-place chol_unblocked on a column-major buffer, column-ordered
+    evaluation (bit-identical to chol); returns the info code (0, or the failing 1-based column)."""
+    return lib().or_chol_unblocked_cols(n, _p(A_cm), max(1, n))
 
 
 def chol_fwd_symbolic(L, sigma_dot):

@@ -27,6 +27,34 @@
 
 #define E(M, i, j, ld) ((M)[(size_t)(j) * (size_t)(ld) + (size_t)(i)])
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* [lo, hi) split into one contiguous range per OpenMP thread (the whole range outside a
+ * parallel region).  Scheduling only: no arithmetic of the method. */
+static void row_range(int64_t lo, int64_t hi, int64_t* i0, int64_t* i1) {
+  int64_t nt = 1, t = 0;
+#ifdef _OPENMP
+  nt = omp_get_num_threads();
+  t = omp_get_thread_num();
+#endif
+  const int64_t len = hi - lo, per = (len + nt - 1) / nt;
+  *i0 = lo + t * per < hi ? lo + t * per : hi;
+  *i1 = *i0 + per < hi ? *i0 + per : hi;
+}
+
+/* Thread count of the OpenMP regions below (bench.py times the single-matrix oracle on one
+ * thread); 0 or less restores the default.  Scheduling only. */
+void or_set_threads(int t) {
+#ifdef _OPENMP
+  if (t > 0) omp_set_num_threads(t);
+  else omp_set_num_threads(omp_get_num_procs());
+#else
+  (void)t;
+#endif
+}
+
 /* ------------------------------------------------------------------------- */
 /* chol_unblocked (DPOTF2).  In place: tril(A)=tril(Sigma)  */
 /* -> tril(A)=L.  Returns 0, or j+1 (1-based) if d - r r^T <= 0 at column j.  */
@@ -47,6 +75,53 @@ int or_chol_unblocked(int64_t n, double* A, int64_t lda) {
     }
   }
   return 0;
+}
+
+/* or_chol_unblocked with the row loop innermost (column walks; for the large-n
+ * parity tests).  Each sum B r^T starts at 0.0 and adds m = 0..j-1 in order, so
+ * the result is bit-identical to or_chol_unblocked (test_chol_cols_bit_identical).
+ * Rows are independent given d: OpenMP over row ranges. */
+int or_chol_unblocked_cols(int64_t n, double* A, int64_t lda) {
+  double* t = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  int ret = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    /* d <- sqrt(d - r r^T) */
+    double s = E(A, j, j, lda);
+    for (int64_t m = 0; m < j; ++m) s -= E(A, j, m, lda) * E(A, j, m, lda);
+    if (!(s > 0.0)) { ret = (int)(j + 1); break; }
+    const double d = sqrt(s);
+    E(A, j, j, lda) = d;
+    /* c <- (c - B r^T) / d */
+    /* one contiguous row range per thread, m outermost, four terms per pass in the same
+     * left-to-right order (see or_chol_fwd_cols) */
+    const int64_t rows = n - j - 1;
+#pragma omp parallel if (rows * j >= (1 << 16))
+    {
+      int64_t i0, i1;
+      row_range(j + 1, n, &i0, &i1);
+      for (int64_t i = i0; i < i1; ++i) t[i] = 0.0;
+      int64_t m = 0;
+      for (; m + 4 <= j; m += 4) {
+        const double r0 = E(A, j, m, lda), r1 = E(A, j, m + 1, lda), r2 = E(A, j, m + 2, lda),
+                     r3 = E(A, j, m + 3, lda);
+        for (int64_t i = i0; i < i1; ++i) {
+          double a = t[i];
+          a += E(A, i, m, lda) * r0;
+          a += E(A, i, m + 1, lda) * r1;
+          a += E(A, i, m + 2, lda) * r2;
+          a += E(A, i, m + 3, lda) * r3;
+          t[i] = a;
+        }
+      }
+      for (; m < j; ++m) {
+        const double r_m = E(A, j, m, lda);
+        for (int64_t i = i0; i < i1; ++i) t[i] += E(A, i, m, lda) * r_m;
+      }
+      for (int64_t i = i0; i < i1; ++i) E(A, i, j, lda) = (E(A, i, j, lda) - t[i]) / d;
+    }
+  }
+  free(t);
+  return ret;
 }
 
 /* Same algorithm over complex numbers, for complex-step differentiation
@@ -92,6 +167,73 @@ int or_chol_fwd(int64_t n, const double* L, int64_t ldl, double* Ad, int64_t lda
     }
   }
   return 0;
+}
+
+/* The same statements as or_chol_fwd, evaluated with the  */
+/* loop over rows i innermost so that every access walks down a column (the   */
+/* column-major layout) -- the only use is large n (full-size parity tests,   */
+/* N = 16384), where or_chol_fwd's row-wise walk through a 2 GiB array is     */
+/* TLB-bound.  Each sum Bdot r^T, B rdot^T still starts at 0.0 and adds the   */
+/* terms m = 0, 1, ..., j-1 in that order, and every other operation is the   */
+/* same, so the result is bit-identical to or_chol_fwd (test_oracle.py::      */
+/* test_fwd_cols_bit_identical).  Rows i are independent given ddot: OpenMP   */
+/* over row ranges.  t1/t2: caller-free scratch of n doubles each.            */
+int or_chol_fwd_cols(int64_t n, const double* L, int64_t ldl, double* Ad, int64_t lda) {
+  double* t1 = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  double* t2 = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  int ret = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    double d = E(L, j, j, ldl);
+    if (d == 0.0 || !isfinite(d)) { ret = (int)(j + 1); break; }
+    /* ddot <- (ddot/2 - r rdot^T) / d */
+    double r_rdot = 0.0;
+    for (int64_t m = 0; m < j; ++m) r_rdot += E(L, j, m, ldl) * E(Ad, j, m, lda);
+    const double ddot = (E(Ad, j, j, lda) / 2.0 - r_rdot) / d;
+    E(Ad, j, j, lda) = ddot;
+    /* cdot <- (cdot - Bdot r^T - B rdot^T - c ddot) / d */
+    /* rows j+1..n-1 split into one contiguous range per thread; within a range the m loop
+     * is outermost (column walks) and the per-row sums t1, t2 stay in cache.  Four terms per
+     * pass: t = ((t + a_m r_m) + a_{m+1} r_{m+1}) + ...  -- the same left-to-right order. */
+    const int64_t rows = n - j - 1;
+#pragma omp parallel if (rows * j >= (1 << 16))
+    {
+      int64_t i0, i1;
+      row_range(j + 1, n, &i0, &i1);
+      for (int64_t i = i0; i < i1; ++i) { t1[i] = 0.0; t2[i] = 0.0; }
+      int64_t m = 0;
+      for (; m + 4 <= j; m += 4) {
+        const double r0 = E(L, j, m, ldl), r1 = E(L, j, m + 1, ldl), r2 = E(L, j, m + 2, ldl),
+                     r3 = E(L, j, m + 3, ldl);
+        const double q0 = E(Ad, j, m, lda), q1 = E(Ad, j, m + 1, lda), q2 = E(Ad, j, m + 2, lda),
+                     q3 = E(Ad, j, m + 3, lda);
+        for (int64_t i = i0; i < i1; ++i) {
+          double a = t1[i], b = t2[i];
+          a += E(Ad, i, m, lda) * r0;     /* Bdot r^T  */
+          a += E(Ad, i, m + 1, lda) * r1;
+          a += E(Ad, i, m + 2, lda) * r2;
+          a += E(Ad, i, m + 3, lda) * r3;
+          b += E(L, i, m, ldl) * q0;      /* B rdot^T  */
+          b += E(L, i, m + 1, ldl) * q1;
+          b += E(L, i, m + 2, ldl) * q2;
+          b += E(L, i, m + 3, ldl) * q3;
+          t1[i] = a;
+          t2[i] = b;
+        }
+      }
+      for (; m < j; ++m) {
+        const double r_m = E(L, j, m, ldl), rdot_m = E(Ad, j, m, lda);
+        for (int64_t i = i0; i < i1; ++i) {
+          t1[i] += E(Ad, i, m, lda) * r_m;
+          t2[i] += E(L, i, m, ldl) * rdot_m;
+        }
+      }
+      for (int64_t i = i0; i < i1; ++i)
+        E(Ad, i, j, lda) = (E(Ad, i, j, lda) - t1[i] - t2[i] - E(L, i, j, ldl) * ddot) / d;
+    }
+  }
+  free(t1);
+  free(t2);
+  return ret;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -156,6 +298,15 @@ void or_chol_fwd_batched(int64_t n, int64_t batch, const double* L, int64_t ldl,
 #pragma omp parallel for schedule(dynamic, 16)
   for (int64_t b = 0; b < batch; ++b)
     info[b] = or_chol_fwd(n, L + b * sL, ldl, Ad + b * sA, lda);
+}
+
+/* As or_chol_fwd_batched with the column-ordered evaluation (bit-identical, see
+ * or_chol_fwd_cols; its inner OpenMP region stays serial inside this one). */
+void or_chol_fwd_cols_batched(int64_t n, int64_t batch, const double* L, int64_t ldl, int64_t sL,
+                              double* Ad, int64_t lda, int64_t sA, int* info) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t b = 0; b < batch; ++b)
+    info[b] = or_chol_fwd_cols(n, L + b * sL, ldl, Ad + b * sA, lda);
 }
 
 /* ------------------------------------------------------------------------- */

@@ -9,7 +9,18 @@ Arguments are torch CUDA tensors (float64 or float32) holding one (N, N) matrix 
 a batch (B, N, N), in *logical* orientation with COLUMN-MAJOR memory per matrix,
 i.e. ``t.stride(-2) == 1`` (``colmajor(t)`` makes such a copy).  Only lower
 triangles are read.  The computation is in place on the second argument (as in
-the paper) unless ``inplace=False``.
+the paper) unless ``inplace=False``: a column-major second argument is updated
+directly; any other layout is processed in a column-major copy whose result is
+copied back into the caller's tensor, so the in-place contract holds for every
+layout (the returned tensor is always the caller's).
+
+Numerical status (SPEC.md's SingularFactorError; include/choldiff.h d_info) is
+asynchronous: ``info=True`` returns the per-matrix status tensor without a
+synchronisation; ``check=True`` synchronises and raises
+:class:`SingularFactorError` when some L[j, j] is zero or non-finite.  The
+default (neither) never synchronises, so the calls can be captured in CUDA
+graphs and timed back to back; a singular factor then yields unspecified
+(non-finite) outputs.
 
 This module only marshals arguments (pointers, leading dimensions, the current
 torch stream and a workspace tensor) into the C ABI; every arithmetic step runs in
@@ -28,7 +39,7 @@ from . import _build
 
 __all__ = ["chol_rev", "chol_fwd", "chol_host", "colmajor", "workspace_size", "lib", "library_path",
            "launch_count", "reset_launch_count", "CholdiffError", "OUT_MODES", "ROUTES", "host_bytes",
-           "chol_fwd_fused"]
+           "chol_fwd_fused", "chol_rev_fwd", "SingularFactorError"]
 
 CD_F64, CD_F32 = 0, 1
 CD_OP_REV, CD_OP_FWD, CD_OP_CHOL_FWD = 0, 1, 2
@@ -41,6 +52,15 @@ _lock = threading.Lock()
 
 class CholdiffError(RuntimeError):
     pass
+
+
+class SingularFactorError(CholdiffError, ValueError):
+    """A diagonal entry L[j, j] is zero or non-finite (``.info``: per-matrix 1-based index, 0 = ok)."""
+
+    def __init__(self, info):
+        self.info = info
+        bad = [(b, int(v)) for b, v in enumerate(info) if v]
+        super().__init__(f"singular factor: (matrix, 1-based column) {bad[:8]}{' ...' if len(bad) > 8 else ''}")
 
 
 class _Opts(ctypes.Structure):
@@ -178,6 +198,8 @@ def workspace_size(op: str, dtype: torch.dtype, n: int, batch: int = 1, nb=None,
 
 
 def _prep(L: torch.Tensor, A: torch.Tensor, inplace: bool):
+    """Returns (L, A, dest): column-major operands, and the caller's tensor to copy the
+    result back into when an in-place call had to work on a column-major copy (else None)."""
     if not (L.is_cuda and A.is_cuda):
         raise CholdiffError("chol_rev/chol_fwd take CUDA tensors (use chol_host for host buffers)")
     if L.dtype != A.dtype:
@@ -186,17 +208,32 @@ def _prep(L: torch.Tensor, A: torch.Tensor, inplace: bool):
         raise ValueError(f"expected matching (N,N) or (B,N,N) tensors, got {tuple(L.shape)} / {tuple(A.shape)}")
     if not is_colmajor(L):
         L = colmajor(L)
-    if not inplace or not is_colmajor(A):
+    dest = None
+    if not inplace:
         A = colmajor(A)
-    return L, A
+    elif not is_colmajor(A):
+        dest, A = A, colmajor(A)
+    return L, A, dest
+
+
+def _finish(A: torch.Tensor, dest, info_t, info: bool, check: bool):
+    if dest is not None:
+        dest.copy_(A)  # in-place contract for non-column-major sensitivities
+        A = dest
+    if check and info_t is not None:
+        host = info_t.cpu()  # synchronises the current stream
+        if bool(host.any()):
+            raise SingularFactorError(host.tolist())
+    return (A, info_t) if info else A
 
 
 def _run(op: int, L: torch.Tensor, A: torch.Tensor, nb, route, out, info: bool):
+    """One C-ABI call; returns (A, info tensor or None)."""
     Lc = lib()
     n = A.shape[-1]
     batch = A.shape[0] if A.dim() == 3 else 1
     if n == 0 or batch == 0:  # no-op (the C ABI returns CD_SUCCESS as well)
-        return (A, torch.zeros(batch, dtype=torch.int32, device=A.device)) if info else A
+        return A, (torch.zeros(batch, dtype=torch.int32, device=A.device) if info else None)
     o = _opts(nb, route, out)
     dt = _dt(A)
     dev = A.device
@@ -222,23 +259,27 @@ def _run(op: int, L: torch.Tensor, A: torch.Tensor, nb, route, out, info: bool):
             rc = f(dt, n, L.data_ptr(), ldl, sL, A.data_ptr(), lda, sA, batch, ctypes.byref(o), wsp, nbytes, ip,
                    stream)
         _check(rc)
-    return (A, info_t) if info else A
+    return A, info_t
 
 
 def chol_rev(L: torch.Tensor, Lbar: torch.Tensor, *, nb=None, route: str = "auto", out: str = "tril",
-             inplace: bool = True, info: bool = False):
+             inplace: bool = True, info: bool = False, check: bool = False):
     """Reverse mode (L, Lbar) -> Sigma_bar.  Returns the tensor holding tril(Sigma_bar)
     (Eq. 10 convention; ``out='sym'`` / ``'grad'`` also write the upper triangle, see
-    include/choldiff.h).  With ``info=True`` also returns the per-matrix status tensor."""
-    L, A = _prep(L, Lbar, inplace)
-    return _run(CD_OP_REV, L, A, nb, route, out, info)
+    include/choldiff.h).  With ``info=True`` also returns the per-matrix status tensor;
+    ``check=True`` synchronises and raises SingularFactorError on a singular factor."""
+    L, A, dest = _prep(L, Lbar, inplace)
+    A, info_t = _run(CD_OP_REV, L, A, nb, route, out, info or check)
+    return _finish(A, dest, info_t, info, check)
 
 
 def chol_fwd(L: torch.Tensor, Sdot: torch.Tensor, *, nb=None, route: str = "auto", inplace: bool = True,
-             info: bool = False):
-    """Forward mode (L, Sigma_dot) -> L_dot (lower triangle of the returned tensor)."""
-    L, A = _prep(L, Sdot, inplace)
-    return _run(CD_OP_FWD, L, A, nb, route, "tril", info)
+             info: bool = False, check: bool = False):
+    """Forward mode (L, Sigma_dot) -> L_dot (lower triangle of the returned tensor).
+    ``info`` / ``check`` as for chol_rev."""
+    L, A, dest = _prep(L, Sdot, inplace)
+    A, info_t = _run(CD_OP_FWD, L, A, nb, route, "tril", info or check)
+    return _finish(A, dest, info_t, info, check)
 
 
 def chol_rev_fwd(L: torch.Tensor, Lbar: torch.Tensor, Sdot: torch.Tensor, *, nb=None, inplace: bool = True):
@@ -246,8 +287,8 @@ def chol_rev_fwd(L: torch.Tensor, Lbar: torch.Tensor, Sdot: torch.Tensor, *, nb=
     (cd_chol_rev_fwd_strided_batched): Sigma_bar = chol_rev(L, Lbar) and L_dot = chol_fwd(L, Sdot),
     the two independent sweeps on two streams inside the library, ordered on the current stream.
     Returns (Sigma_bar, L_dot)."""
-    Lc, A = _prep(L, Lbar, inplace)
-    _, F = _prep(Lc, Sdot, inplace)
+    Lc, A, dA = _prep(L, Lbar, inplace)
+    _, F, dF = _prep(Lc, Sdot, inplace)
     if F.shape != A.shape or F.dtype != A.dtype:
         raise ValueError("Lbar and Sdot must match")
     Lk = lib()
@@ -269,6 +310,12 @@ def chol_rev_fwd(L: torch.Tensor, Lbar: torch.Tensor, Sdot: torch.Tensor, *, nb=
                                                 F.data_ptr(), ld(F), sb(F), batch, ctypes.byref(o), wsp, nbytes,
                                                 None, stream)
         _check(rc)
+    if dA is not None:
+        dA.copy_(A)
+        A = dA
+    if dF is not None:
+        dF.copy_(F)
+        F = dF
     return A, F
 
 
@@ -282,8 +329,8 @@ def chol_fwd_fused(Sigma: torch.Tensor, Sdot: torch.Tensor, *, info: bool = Fals
     A, Ad = Sigma, Sdot
     if not (A.is_cuda and Ad.is_cuda) or A.shape != Ad.shape or A.dtype != Ad.dtype:
         raise ValueError("chol_fwd_fused takes two CUDA tensors of the same shape and dtype")
-    r = _run(CD_OP_CHOL_FWD, A, Ad, None, "auto", "tril", info)
-    return (A, r[0], r[1]) if info else (A, r)
+    Ad, info_t = _run(CD_OP_CHOL_FWD, A, Ad, None, "auto", "tril", info)
+    return (A, Ad, info_t) if info else (A, Ad)
 
 
 def chol_host(op: str, L_host: torch.Tensor, A_host: torch.Tensor, *, nb=None, device=None) -> torch.Tensor:

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -43,6 +44,23 @@
 
 namespace cd {
 
+// ---- per-device caches of launch attributes (occupancies, SM counts): a process may drive
+// several devices (or MIG slices) with different SM counts.  Computed on first use per device;
+// the computation is idempotent, so a race only computes the same value twice. ----
+constexpr int kMaxDev = 64;
+constexpr int64_t kGridBatch = 32768;  // batch chunk of the paths with the matrix index on grid.y/z
+template <typename F>
+static int per_device(std::atomic<int> (&cache)[kMaxDev], F&& compute) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return compute();
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    v = compute();
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 static thread_local int64_t g_launches = 0;
 static thread_local char g_cuda_err[256] = "";
 
@@ -65,6 +83,9 @@ struct Prof {
     }
     return pool[used++];
   }
+  ~Prof() {  // thread exit: release this thread's events (errors ignored at process teardown)
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
 };
 static thread_local Prof g_prof;
 
@@ -81,6 +102,11 @@ struct LaStreams {
       pool.push_back(e);
     }
     return pool[next++];
+  }
+  ~LaStreams() {  // thread exit: release this thread's streams and events
+    if (chain) cudaStreamDestroy(chain);
+    if (bulk) cudaStreamDestroy(bulk);
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
   }
 };
 static thread_local LaStreams g_la[64];
@@ -129,6 +155,9 @@ struct HostPipe {
     return pool[next++];
   }
   size_t off(int64_t r, int64_t c) const { return (size_t(r) + size_t(c) * size_t(n)) * es; }
+  ~HostPipe() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
   // diagonal blocks of L first (the block inverses need all of them), then column blocks in
   // the order `order` lists them; returns one event per column block
   void h2d(int nblk, int nb, bool reverse, std::vector<cudaEvent_t>& ev_in, cudaEvent_t& ev_diag);
@@ -147,6 +176,10 @@ static thread_local HostPipe* g_pipe = nullptr;
 struct HostStreams {
   cudaStream_t cin = nullptr, cout = nullptr;
   HostPipe pipe;
+  ~HostStreams() {  // thread exit: release this thread's copy streams
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
+  }
 };
 static thread_local HostStreams g_hs[64];
 static bool g_no_host_pipe = getenv("CD_NO_HOST_PIPE") != nullptr;
@@ -507,13 +540,14 @@ struct Gemm {
   bool launch_tc32_k(int64_t units, const TmaMaps& tm, const TcEpiMaps& em) {
     auto kern = k_gemm_tc32<A_, B_, EPI, STG, BN>;
     constexpr size_t smem = tc_smem(STG, EPI, BN);
-    static int occ = 0;  // per instantiation
-    if (!occ) {
+    static std::atomic<int> occ_cache[kMaxDev];  // per instantiation and device
+    const int occ = per_device(occ_cache, [&] {
+      int o = 0;
       set_smem(kern, smem);
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, tcp_threads(EPI), smem) != cudaSuccess || occ < 1)
-        occ = 1;
-      occ = std::min(occ, 2);  // TMEM: 2 x 256 columns per CTA
-    }
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, tcp_threads(EPI), smem) != cudaSuccess || o < 1)
+        o = 1;
+      return std::min(o, 2);  // TMEM: 2 x 256 columns per CTA
+    });
     set_smem(kern, smem);
     // persistent: a grid of (up to) occ CTAs per SM loops over the units
     const unsigned g = unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(c.sms) * occ)));
@@ -866,14 +900,15 @@ static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DE
 static int64_t g_fs_pieces = getenv("CD_FS_PIECES") ? atoi(getenv("CD_FS_PIECES")) : 16;
 static bool g_no_bal1 = getenv("CD_NO_BAL1") != nullptr;  // forward panel: one CTA per 128-wide K chunk
 
+static std::atomic<int> g_panel_occ[kMaxDev];
 static int panel_occupancy() {
-  static int occ = 0;
-  if (!occ) {
+  return per_device(g_panel_occ, [] {
+    int occ = 0;
     set_smem(k_panel_rev, PR_SMEM);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_panel_rev, PR_THREADS, PR_SMEM) != cudaSuccess || occ < 1)
       occ = 1;
-  }
-  return occ;
+    return occ;
+  });
 }
 
 static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info, double* part_ws) {
@@ -1140,14 +1175,15 @@ static void blocked_fwd(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
 //       (Eq. 8) + the clean copy Dc
 //   k_fwd_sk (stream-K):   W = Cdot - [Bdot B C] [R Rdot Dc]^T, in place
 // The last panel has no rows below it, so no W D^{-T} is left pending.
+static std::atomic<int> g_panel_fwd_occ[kMaxDev];
 static int panel_fwd_occupancy() {
-  static int occ = 0;
-  if (!occ) {
+  return per_device(g_panel_fwd_occ, [] {
+    int occ = 0;
     set_smem(k_panel_fwd, PR_SMEM);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_panel_fwd, PR_THREADS, PR_SMEM) != cudaSuccess || occ < 1)
       occ = 1;
-  }
-  return occ;
+    return occ;
+  });
 }
 
 static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, int* info) {
@@ -1486,7 +1522,7 @@ static int default_nb(cd_dtype dt, int64_t n) {
 }
 
 template <typename T>
-static void drive(Ctx& c, const Call& k) {
+static void drive_one(Ctx& c, const Call& k) {
   const int n = int(k.n);
   if (n == 0 || k.batch == 0) return;
   if (k.op == CD_OP_CHOL_FWD) {  // fused factorisation + forward (fp64; checked with the arguments)
@@ -1661,16 +1697,48 @@ static void drive(Ctx& c, const Call& k) {
   }
 }
 
-static int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-      cached = v;
-    else
-      cached = 148;
+static std::atomic<int> g_sm_count[kMaxDev];
+// Paths whose kernels put the matrix index on gridDim.y / .z (the blocked sweeps' GEMMs and
+// inverses, the fused factorisation's diagonal kernel) run batches above the 65535 grid limit in
+// chunks of kGridBatch matrices, reusing one chunk's workspace; the n <= DC_NMAX on-chip paths
+// index matrices by gridDim.x and take any batch in one launch.
+static Opnd shift_batch(const Opnd& o, int64_t b0, size_t es) {
+  Opnd r = o;
+  if (r.arr) r.arr += b0;
+  else r.base = static_cast<const char*>(r.base) + size_t(b0) * size_t(r.stride) * es;
+  return r;
+}
+
+template <typename T>
+static void drive(Ctx& c, const Call& k) {
+  const bool grid2d = k.op == CD_OP_CHOL_FWD || k.n > DC_NMAX;
+  if (k.batch <= 65535 || !grid2d) {
+    drive_one<T>(c, k);
+    return;
   }
-  return cached;
+  const size_t o0 = c.off;
+  size_t hi = o0;
+  for (int64_t b0 = 0; b0 < k.batch && c.ok(); b0 += kGridBatch) {
+    Call s = k;
+    s.batch = std::min<int64_t>(kGridBatch, k.batch - b0);
+    s.L = shift_batch(k.L, b0, sizeof(T));
+    s.A = shift_batch(k.A, b0, sizeof(T));
+    s.info = k.info ? k.info + b0 : nullptr;
+    c.off = o0;
+    drive_one<T>(c, s);
+    hi = std::max(hi, c.off);
+    if (c.plan) break;  // the first chunk is the largest: it sizes the workspace
+  }
+  c.off = hi;
+}
+
+static int sm_count() {
+  return per_device(g_sm_count, [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      v = 148;
+    return v;
+  });
 }
 
 // ------------------------------------------------------------------ distributed reverse steps
@@ -1930,14 +1998,21 @@ int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t l
 }
 
 // ---- both sweeps of one factor on two streams (cd_chol_rev_fwd_strided_batched) ----
-static thread_local cudaStream_t g_side[64];
-static thread_local std::vector<cudaEvent_t> g_side_ev[64];
+struct SideStream {  // per device and host thread; released at thread exit
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> ev;
+  ~SideStream() {
+    if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+static thread_local SideStream g_side[64];
 
 // the batched fp32 right-looking drivers share one set of diagonal-block inverses (configs[3])
 static int shared_dinv_nb(cd_dtype dt, int64_t n, int64_t batch, const cd_opts& o) {
   const int nb = int(std::min<int64_t>(n, o.nb > 0 ? o.nb : default_nb(dt, n)));
-  const bool ok = dt == CD_F32 && batch > 1 && n > DC_NMAX && nb <= DC_NMAX && n % nb == 0 &&
-                  o.route != CD_ROUTE_SYMBOLIC;
+  const bool ok = dt == CD_F32 && batch > 1 && batch <= kGridBatch && n > DC_NMAX && nb <= DC_NMAX &&
+                  n % nb == 0 && o.route != CD_ROUTE_SYMBOLIC;
   return ok ? nb : 0;
 }
 
@@ -1991,14 +2066,14 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
   if (need > 0 && (!ws || ws_bytes < need)) return -14;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CD_ERR_CUDA;
-  if (!g_side[dev] && (r = note_cuda(cudaStreamCreateWithFlags(&g_side[dev], cudaStreamNonBlocking)))) return r;
-  std::vector<cudaEvent_t>& evs = g_side_ev[dev];
+  if (!g_side[dev].s && (r = note_cuda(cudaStreamCreateWithFlags(&g_side[dev].s, cudaStreamNonBlocking)))) return r;
+  std::vector<cudaEvent_t>& evs = g_side[dev].ev;
   if (evs.empty()) {
     evs.resize(2);
     for (auto& e : evs)
       if ((r = note_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)))) return r;
   }
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream), side = g_side[dev];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream), side = g_side[dev].s;
   const int snb = shared_dinv_nb(dt, n, batch, o);
   if (snb) {  // the inverses of the shared factor, once, before the two sweeps fork
     Ctx c;

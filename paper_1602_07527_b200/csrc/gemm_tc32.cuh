@@ -9,7 +9,7 @@
 //   warp 6        : (EPI >= 1) the epilogue's TMA warp: prefetches Cin chunks into smem slots
 //                   and stores finished chunks with cp.async.bulk.tensor (EPI = 2: transposed,
 //                   through 32 x 128 boxes with the 128-byte swizzle)
-//   last 8 warps  : round each landed operand stage to tf32 in place (cvt.rna) -- SURVEY c11:
+//   last TC_CONVW (8) warps : round each landed operand stage to tf32 in place (cvt.rna) -- SURVEY c11:
 //                   the MMA would otherwise truncate the low 13 mantissa bits (biased error;
 //                   rounding cut the batched N = 512 error 4.3e-5 -> 1.1e-5 against the 1e-4 gate)
 //
@@ -102,9 +102,21 @@ __device__ __forceinline__ float4 tf32_rna4(float4 v) {
   return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
 }
 
+// Protocol-error watchdog of the mbarrier waits: a wait that has not completed after
+// CD_WATCHDOG_NS nanoseconds of wall time (globaltimer) traps instead of hanging the GPU.  Bounded
+// by elapsed time, not by a spin count, so legitimately slow runs (compute-sanitizer, debuggers,
+// time slicing, concurrent streams) never trip it; -DCD_WATCHDOG_NS=0 compiles it out.
+#ifndef CD_WATCHDOG_NS
+#define CD_WATCHDOG_NS 20000000000ull
+#endif
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
-  // bounded wait: a protocol error becomes a trap instead of a hung GPU
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (true) {
     uint32_t ok;
     asm volatile(
@@ -115,7 +127,11 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
     if (ok) return;
-    if (++spins > (1u << 26)) __trap();
+    if (CD_WATCHDOG_NS != 0 && (++spins & 0xFFFFu) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > uint64_t(CD_WATCHDOG_NS)) __trap();
+    }
   }
 }
 
@@ -128,8 +144,8 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
 // so TMEM allocation, barrier setup and the epilogue of one unit overlap the next unit's
 // loads and MMAs (the batched updates are tens of thousands of short-K tiles).
 constexpr int TCP_THREADS = 192;
-// EPI = 1 adds warp 6: the epilogue's TMA warp (Cin prefetch + output stores).  The last four
-// warps round every operand stage to tf32 in place (cvt.rna) before the MMA reads it.
+// EPI = 1 adds warp 6: the epilogue's TMA warp (Cin prefetch + output stores).  The last
+// TC_CONVW (8) warps round every operand stage to tf32 in place (cvt.rna) before the MMA reads it.
 #ifndef CD_TC_EPI_MINB
 #define CD_TC_EPI_MINB 1
 #endif

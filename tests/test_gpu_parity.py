@@ -100,6 +100,95 @@ def test_pointer_array_batched(n):
     assert nerr(out, oracle_rev(L, Lb)) < TOL64
 
 
+@pytest.mark.parametrize("n,dt", [(9, 0), (32, 0), (96, 0), (140, 0), (300, 0), (64, 1), (200, 1)])
+def test_pointer_array_batched_fwd(n, dt):
+    # cd_chol_fwd_batched: device array of device pointers
+    B = 5
+    tdt = torch.float64 if dt == 0 else torch.float32
+    L, _, Sd = synthetic.draw_batch(n, B, seed=7 * n + dt, lbar=False, sdot=True)
+    if dt == 1:
+        L, Sd = fp32_round(L, Sd)
+    Ls = [to_dev(L[b], tdt) for b in range(B)]
+    Fs = [to_dev(np.tril(Sd[b]), tdt) for b in range(B)]
+    lp = torch.tensor([t.data_ptr() for t in Ls], dtype=torch.int64, device="cuda")
+    fp = torch.tensor([t.data_ptr() for t in Fs], dtype=torch.int64, device="cuda")
+    nbytes = cd.workspace_size("fwd", tdt, n, B)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+    info = torch.full((B,), -1, dtype=torch.int32, device="cuda")
+    rc = cd.lib().cd_chol_fwd_batched(dt, n, lp.data_ptr(), n, fp.data_ptr(), n, B, None, ws.data_ptr(), nbytes,
+                                      info.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    assert not info.cpu().any()
+    out = np.stack([to_host(f) for f in Fs])
+    assert nerr(out, oracle_fwd(L, Sd)) < (TOL64 if dt == 0 else TOL32)
+
+
+def test_inplace_non_colmajor_sensitivity_is_updated():
+    # a row-major (ordinary contiguous) sensitivity is processed in a column-major copy
+    # and the result copied back, so the in-place contract holds for every layout
+    n = 150
+    L, Lb, Sd = synthetic.draw(n, 12, sdot=True)
+    Lt = to_dev(L)
+    A_rm = torch.from_numpy(np.ascontiguousarray(Lb)).cuda()  # logical orientation, row-major memory
+    r = cd.chol_rev(Lt, A_rm)
+    assert r.data_ptr() == A_rm.data_ptr()
+    assert nerr(to_host(A_rm), oracle.chol_rev(L, Lb)) < TOL64
+    F_rm = torch.from_numpy(np.ascontiguousarray(np.tril(Sd))).cuda()
+    f = cd.chol_fwd(Lt, F_rm)
+    assert f.data_ptr() == F_rm.data_ptr()
+    assert nerr(to_host(F_rm), oracle_fwd(L, Sd)) < TOL64
+    keep = torch.from_numpy(np.ascontiguousarray(Lb)).cuda()
+    out = cd.chol_rev(Lt, keep, inplace=False)
+    assert torch.equal(keep.cpu(), torch.from_numpy(Lb))  # untouched
+    assert nerr(to_host(out), oracle.chol_rev(L, Lb)) < TOL64
+
+
+def test_check_raises_singular_factor():
+    n = 200
+    L, Lb, _ = synthetic.draw_batch(n, 3, seed=3)
+    L[1, 57, 57] = 0.0
+    with pytest.raises(cd.SingularFactorError) as e:
+        cd.chol_rev(to_dev(L), to_dev(Lb), check=True)
+    assert e.value.info == [0, 58, 0]
+    with pytest.raises(cd.SingularFactorError):
+        cd.chol_fwd(to_dev(L), to_dev(Lb), check=True)
+    L[1, 57, 57] = 1.5
+    cd.chol_rev(to_dev(L), to_dev(Lb), check=True)  # no error
+
+
+@pytest.mark.parametrize("n,op", [(129, "rev"), (129, "fwd"), (130, "fused")])
+def test_batch_above_grid_limit(n, op):
+    # batches above 65535 on the paths whose kernels index matrices by gridDim.y/z
+    # (blocked GEMMs, block inverses, the fused factorisation) run in chunks; spot-check matrices
+    # in the first, second and third chunk against the oracle
+    B = 65536 + 37
+    L1, Lb1, Sd1 = synthetic.draw_batch(n, 4, seed=5, sdot=True)
+    idx = np.arange(B) % 4
+    picks = [0, 32767, 32768, 65535, 65536, B - 1]
+    if op == "fused":
+        Sig = np.einsum("bij,bkj->bik", L1, L1)
+        A = to_dev(Sig)[torch.from_numpy(idx).cuda()]
+        Ad = to_dev(np.tril(Sd1))[torch.from_numpy(idx).cuda()]
+        A, Ad = cd.colmajor(A), cd.colmajor(Ad)
+        Lo, Fo = cd.chol_fwd_fused(A, Ad)
+        for b in picks:
+            Lref = oracle.chol(Sig[idx[b]])
+            assert nerr(to_host(Lo[b]), Lref) < TOL64
+            assert nerr(to_host(Fo[b]), oracle.chol_fwd(Lref, np.tril(Sd1[idx[b]]))) < TOL64
+        return
+    Ld = cd.colmajor(to_dev(L1)[torch.from_numpy(idx).cuda()])
+    if op == "rev":
+        A = cd.colmajor(to_dev(Lb1)[torch.from_numpy(idx).cuda()])
+        out = cd.chol_rev(Ld, A)
+        refs = [oracle.chol_rev(L1[k], Lb1[k]) for k in range(4)]
+    else:
+        A = cd.colmajor(to_dev(np.tril(Sd1))[torch.from_numpy(idx).cuda()])
+        out = cd.chol_fwd(Ld, A)
+        refs = [oracle.chol_fwd(L1[k], np.tril(Sd1[k])) for k in range(4)]
+    for b in picks:
+        assert nerr(to_host(out[b]), refs[idx[b]]) < TOL64
+
+
 @pytest.mark.parametrize("n", [1, 7, 32, 33, 100, 128, 200, 512])
 def test_f32_vs_oracle_on_rounded_inputs(n):
     B = 4

@@ -286,3 +286,37 @@ def test_partial_sweep_is_prefix_of_full():
     oracle.chol_rev_colmajor_inplace(n, Lc, A2, j_lo=0)
     # columns >= jlo are final after the partial sweep (the sweep runs j = N..1)
     assert np.array_equal(A1[jlo:], A2[jlo:])
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 64, 129, 700, 1100])
+def test_fwd_cols_bit_identical(n):
+    # the column-ordered evaluation (large-n parity tests) is the same arithmetic as chol_fwd:
+    # every sum adds its terms in the same order, so the results agree bit for bit
+    L, _, Sd = synthetic.draw(n, 31 + n, lbar=False, sdot=True)
+    ref = oracle.chol_fwd(L, np.tril(Sd))
+    Lc, Ac = synthetic.to_colmajor(L).copy(), synthetic.to_colmajor(np.tril(Sd)).copy()
+    assert oracle.chol_fwd_colmajor_inplace(n, Lc, Ac) == 0
+    assert np.array_equal(np.tril(synthetic.from_colmajor(Ac)), np.tril(ref))
+    B = 3
+    Lb3, _, Sd3 = synthetic.draw_batch(min(n, 64), B, seed=n, lbar=False, sdot=True)
+    m = Lb3.shape[-1]
+    Lc3, Ac3 = synthetic.to_colmajor(Lb3), synthetic.to_colmajor(np.tril(Sd3))
+    assert not oracle.chol_fwd_cols_batched_colmajor(m, B, Lc3, Ac3).any()
+    for b in range(B):
+        assert np.array_equal(np.tril(synthetic.from_colmajor(Ac3[b])), np.tril(oracle.chol_fwd(Lb3[b], np.tril(Sd3[b]))))
+
+
+@pytest.mark.parametrize("n", [1, 3, 64, 600, 1100])
+def test_chol_cols_bit_identical(n):
+    L, _, _ = synthetic.draw(n, 5 + n, lbar=False)
+    S = L @ L.T
+    ref = oracle.chol(S)
+    Sc = synthetic.to_colmajor(S).copy()  # (to_colmajor may alias a 1 x 1 input)
+    assert oracle.chol_colmajor_inplace(n, Sc) == 0
+    assert np.array_equal(np.tril(synthetic.from_colmajor(Sc)), ref)
+    # not positive definite -> the same failing column as chol_unblocked
+    S2 = S.copy()
+    S2[n // 2, n // 2] = -1.0
+    with pytest.raises(oracle.NotPositiveDefinite) as e:
+        oracle.chol(S2)
+    assert oracle.chol_colmajor_inplace(n, synthetic.to_colmajor(S2).copy()) == e.value.j
