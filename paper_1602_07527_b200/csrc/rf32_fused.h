@@ -1,0 +1,34 @@
+// rf32_fused.h -- internal interface (between choldiff.cu and rf32_fused.cu) of the fused
+// per-matrix fp32 batched sweeps (SURVEY §8 row a15, configs[3]).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace cd {
+
+// mode bit 0: reverse sweep (tril(Abar) = Lbar -> tril(Sigma_bar)), bit 1: forward sweep
+// (tril(Adot) = tril(Sigma_dot) -> L_dot), both in place, column-major, fp32.
+struct RF32Call {
+  int mode;
+  int n;
+  int64_t batch;
+  const float* L;
+  int64_t ldl, sL;
+  float* Ab;
+  int64_t lda, sA;
+  float* Ad;
+  int64_t ldd, sD;
+};
+
+// true when the fused kernel handles this call: 128 < n <= 512, n % 64 == 0, 16-byte aligned
+// bases, leading dimensions and batch strides multiples of 4 elements
+bool rf32_fused_supported(const RF32Call& c);
+// device workspace (bytes): the diagonal-block inverses and, for the reverse sweep, the
+// symmetric diagonal blocks S_J = Dbar_J + Dbar_J^T
+size_t rf32_fused_ws(int n, int64_t batch);
+// enqueue on `st`: the block inverses (k_rf_trinv) then the fused sweeps (k_rf32).  Returns
+// cudaSuccess or the launch error; *launches += kernels enqueued.
+cudaError_t rf32_fused_launch(const RF32Call& c, void* ws, cudaStream_t st, int sms, int64_t* launches);
+
+}  // namespace cd
