@@ -353,6 +353,11 @@ static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
 static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
 static int g_tc_bn64 = getenv("CD_TC_BN64") ? atoi(getenv("CD_TC_BN64")) : 1;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
+// fp32 64-wide diagonal blocks of the layered schedule on the mma.sync Eq. 10 / Eq. 8 kernel of
+// rf32_fused.cu (default; configs[3] launch list: 41.6 vs 51.5 us per launch of 1024 blocks) or on
+// the fp64-DMMA on-chip sweeps (CD_NO_HMMA_DIAG=1).  The block inverses stay on k_trinv_dmma
+// (168 us for 8192 blocks; the fp32 forward-substitution kernel k_rf_trinv took 474 us).
+static bool g_no_hmma_diag = getenv("CD_NO_HMMA_DIAG") != nullptr;
 
 // ------------------------------------------------------------------ GEMM launcher
 constexpr int64_t PART_TILES = 2 * 152;  // split-K partial budget, in 128x128 output tiles
@@ -681,6 +686,29 @@ static void run_trinv(Ctx& c, int n, int nb, bool reverse, int64_t batch, Opnd L
   c.launched();
 }
 
+// Diagonal block of a blocked step (PAPER.md:698 / 662): fp32 64-wide blocks of batches on the
+// mma.sync Eq. 10 / Eq. 8 kernel (rf32_fused.cu, uses the block inverse Dinv_q); otherwise the
+// on-chip sweeps of run_sweep_small.
+template <typename T>
+static void diag_block(Ctx& c, bool rev, int w, int64_t batch, Opnd L, Opnd A, Opnd S, Opnd Dinv_q) {
+  if constexpr (sizeof(T) == 4) {
+    if (w == 64 && !L.arr && !A.arr && !S.arr && !g_no_hmma_diag) {
+      if (c.plan || !c.ok()) return;
+      c.pre(CD_PROF_SWEEP, double(batch) * (rev ? (4.0 * w * w * w + 3.0 * w * w + 11.0 * w) / 6
+                                                : (4.0 * w * w * w + 3.0 * w * w + 5.0 * w) / 6));
+      c.err = note_cuda(rf32_diag64(rev, batch, static_cast<const float*>(L.base) + L.off, L.ld, L.stride,
+                                    const_cast<float*>(static_cast<const float*>(A.base)) + A.off, A.ld, A.stride,
+                                    static_cast<const float*>(Dinv_q.base) + Dinv_q.off, Dinv_q.stride,
+                                    S.base ? const_cast<float*>(static_cast<const float*>(S.base)) + S.off : nullptr,
+                                    S.ld, S.stride, c.st));
+      ++g_launches;
+      if (g_prof.on && !g_prof.recs.empty()) cudaEventRecord(g_prof.recs.back().b, c.st);
+      return;
+    }
+  }
+  run_sweep_small<T>(c, rev, w, batch, L, A, 0, S, nullptr);
+}
+
 template <typename T>
 static void run_copy(Ctx& c, int M, int N, int64_t batch, Opnd S, Opnd D) {
   if (c.plan || !c.ok() || M <= 0 || N <= 0) return;
@@ -769,7 +797,7 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
           .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
     }
     // Dbar <- chol_unblocked_rev(D, Dbar)  (+ S = Dbar + Dbar^T)      (w <= DC_NMAX)
-    run_sweep_small<T>(c, true, w, batch, sub(L, j, j), sub(A, j, j), 0, q > 0 ? S : null_opnd(), nullptr);
+    diag_block<T>(c, true, w, batch, sub(L, j, j), sub(A, j, j), q > 0 ? S : null_opnd(), Dinv_q);
     // Rbar <- Rbar - Cbar^T B - (Dbar + Dbar^T) R
     if (q > 0 && rbar_transposed<T>(c, batch, q, w, L, A, j, W)) {
       // fp32 batches: as Rbar^T -= [R; B]^T [S; Cbar] -- M = q rows of 128-row tiles instead of
@@ -1149,7 +1177,7 @@ static void blocked_fwd(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
           .seg(sub(L, j, 0), sub(A, j, 0), q)
           .flops(2.0 * w * (w + 1) * q)  // lower triangle only
           .run(sub(A, j, j), sub(A, j, j), -1.0, 1.0, 1, part_ws);
-    run_sweep_small<T>(c, false, w, batch, sub(L, j, j), sub(A, j, j), 0, p > 0 ? Dc : null_opnd(), nullptr);
+    diag_block<T>(c, false, w, batch, sub(L, j, j), sub(A, j, j), p > 0 ? Dc : null_opnd(), Dinv_q);
     if (p > 0) {
       Gemm<T> g(c, p, w, 0, 1, batch);
       if (q > 0) g.seg(sub(A, k, 0), sub(L, j, 0), q).seg(sub(L, k, 0), sub(A, j, 0), q);

@@ -705,6 +705,85 @@ __global__ void __launch_bounds__(THREADS, 1) k_rf32(const Params p, const __gri
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
+
+// ---------------------------------------------------------------- diagonal blocks of the layered
+// fp32 schedule (N_b = 64): one CTA of 256 threads per matrix, the same Eq. 10 / Eq. 8 products as
+// the fused kernel's R5 / F3 on mma.sync from shared memory (replaces the fp64-DMMA 8 x 8 blocked
+// sweeps k_rev_dmma_cta / k_fwd_dmma_cta for these blocks).
+//   rev: tril(A) = Dbar' -> Dbar = Phi(X), X = D^{-T}(P + P^T)D^{-1}, P = Phi(D^T Dbar');
+//        S (optional, dense) = Dbar + Dbar^T = Phi(X) + Phi(X)^T
+//   fwd: tril(A) = Ddot' -> Ddot = D Phi(D^{-1} Ddot'_sym D^{-T}); S (optional) = tril(Ddot),
+//        zeros above
+struct Diag64 {
+  const float* L;
+  int64_t ldl, sL;
+  float* A;
+  int64_t lda, sA;
+  const float* Dinv;  // 64 x 64 blocks, ld 64, batch stride dstride
+  int64_t dstride;
+  float* S;
+  int64_t lds, sS;
+  int rev;
+};
+__global__ void __launch_bounds__(PANEL_THREADS) k_rf_diag64(const Diag64 q) {
+  extern __shared__ __align__(16) unsigned char smem_d64[];
+  const uint32_t b0 = smem_u32(smem_d64), b1 = b0 + 4 * SCR, b2 = b1 + 4 * SCR, b3 = b2 + 4 * SCR, b4 = b3 + 4 * SCR;
+  const int pt = threadIdx.x, pw = pt >> 5;
+  const int64_t b = blockIdx.x;
+  const float* L = q.L + b * q.sL;
+  float* A = q.A + b * q.sA;
+  float* S = q.S ? q.S + b * q.sS : nullptr;
+  {
+    Tile64 td, ti, ta;
+    td.load(L, q.ldl, pt, true);                     // D
+    ti.load(q.Dinv + b * q.dstride, NBK, pt, false);  // D^{-1}
+    ta.load(A, q.lda, pt, true);                     // Dbar' / Ddot' (lower)
+    td.store(b1, pt);
+    ti.store(b2, pt);
+    ta.store(b0, pt);
+  }
+  panel_sync();
+  if (q.rev) {
+    gemm64(pw, rowmajor(b1).tr(), rowmajor(b0), [&](int r, int c, float v) { sts(el(b3, r, c), v); });  // P
+    panel_sync();
+    for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Psym
+      const int i = e >> 6, j = e & 63;
+      sts(el(b4, i, j), i >= j ? lds(el(b3, i, j)) : lds(el(b3, j, i)));
+    }
+    panel_sync();
+    gemm64(pw, rowmajor(b2).tr(), rowmajor(b4), [&](int r, int c, float v) { sts(el(b3, r, c), v); });  // X1
+    panel_sync();
+    gemm64(pw, rowmajor(b3), rowmajor(b2), [&](int i, int j, float v) {  // X
+      if (i > j) {
+        A[i + int64_t(j) * q.lda] = v;
+        if (S) {
+          S[i + int64_t(j) * q.lds] = v;
+          S[j + int64_t(i) * q.lds] = v;
+        }
+      } else if (i == j) {
+        A[i + int64_t(i) * q.lda] = 0.5f * v;
+        if (S) S[i + int64_t(i) * q.lds] = v;
+      }
+    });
+  } else {
+    for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Ddot'_sym
+      const int i = e >> 6, c = e & 63;
+      sts(el(b3, i, c), i >= c ? lds(el(b0, i, c)) : lds(el(b0, c, i)));
+    }
+    panel_sync();
+    gemm64(pw, rowmajor(b2), rowmajor(b3), [&](int r, int c, float v) { sts(el(b0, r, c), v); });  // Y
+    panel_sync();
+    gemm64(pw, rowmajor(b0), rowmajor(b2).tr(), [&](int r, int c, float v) {  // Z = Phi(Y D^{-T})
+      sts(el(b3, r, c), (r > c) ? v : (r == c ? 0.5f * v : 0.f));
+    });
+    panel_sync();
+    gemm64(pw, rowmajor(b1), rowmajor(b3), [&](int r, int c, float v) {  // Ddot = D Z
+      if (r >= c) A[r + int64_t(c) * q.lda] = v;
+      if (S) S[r + int64_t(c) * q.lds] = r >= c ? v : 0.f;
+    });
+  }
+}
+
 // Block inverses D_J^{-1} (fp32 forward substitution, one CTA of 64 threads per 64 x 64 block;
 // thread c solves D x = e_c with four partial sums).  Out: 64 x n per matrix, column-major.
 __global__ void __launch_bounds__(64) k_rf_trinv(int n, int nblk, const float* __restrict__ L, int64_t ldl,
@@ -862,6 +941,21 @@ cudaError_t rf32_fused_launch(const RF32Call& c, void* ws, cudaStream_t st, int 
   const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((items + nslots - 1) / nslots, sms)));
   k_rf32<<<grid, THREADS, SMEM, st>>>(p, tm);
   ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t rf32_diag64(bool rev, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* A, int64_t lda,
+                        int64_t sA, const float* Dinv, int64_t dstride, float* S, int64_t lds, int64_t sS,
+                        cudaStream_t st) {
+  using namespace rf;
+  Diag64 q{L, ldl, sL, A, lda, sA, Dinv, dstride, S, lds, sS, rev ? 1 : 0};
+  constexpr size_t smem = 5 * SCR * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rf_diag64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  k_rf_diag64<<<unsigned(batch), PANEL_THREADS, smem, st>>>(q);
   return cudaGetLastError();
 }
 

@@ -24,11 +24,19 @@ struct RF32Call {
 // true when the fused kernel handles this call: 128 < n <= 512, n % 64 == 0, 16-byte aligned
 // bases, leading dimensions and batch strides multiples of 4 elements
 bool rf32_fused_supported(const RF32Call& c);
-// device workspace (bytes): the diagonal-block inverses and, for the reverse sweep, the
-// symmetric diagonal blocks S_J = Dbar_J + Dbar_J^T
+// device workspace (bytes): the diagonal-block inverses, the symmetric diagonal blocks
+// S_J = Dbar_J + Dbar_J^T and the tf32-rounded shadows L_r, T_r, Ldot_r
 size_t rf32_fused_ws(int n, int64_t batch);
 // enqueue on `st`: the block inverses (k_rf_trinv) then the fused sweeps (k_rf32).  Returns
 // cudaSuccess or the launch error; *launches += kernels enqueued.
 cudaError_t rf32_fused_launch(const RF32Call& c, void* ws, cudaStream_t st, int sms, int64_t* launches);
+
+// The layered fp32 schedule's diagonal-block update of one 64-wide panel for every matrix of a batch
+// (rev: Eq. 10 -> tril(Dbar), S = Dbar + Dbar^T dense; fwd: Eq. 8 -> tril(Ddot), S = tril(Ddot) with
+// zeros above; S may be null), given the block inverses (64 x 64, ld 64, batch stride dstride).
+// A / L / S point at the diagonal block of matrix 0.
+cudaError_t rf32_diag64(bool rev, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* A, int64_t lda,
+                        int64_t sA, const float* Dinv, int64_t dstride, float* S, int64_t lds, int64_t sS,
+                        cudaStream_t st);
 
 }  // namespace cd
