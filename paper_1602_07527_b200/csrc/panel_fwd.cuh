@@ -63,8 +63,11 @@ __device__ __forceinline__ void pf_prod128(double* sm, int K, FA fa, FB fb, SK s
       const int kk = kc * 16 + kx;
       const double* pa = kk < K ? fa(m, kk) : nullptr;
       const double* pb = kk < K ? fb(kk, m) : nullptr;
-      cp_async8(as + kx * P + m, pa ? pa : as, pa != nullptr);
-      cp_async8(bs + kx * P + m, pb ? pb : bs, pb != nullptr);
+      // no source -> a zero by a plain shared store (never a zero-size copy from a dummy address)
+      if (pa) cp_async8(as + kx * P + m, pa, true);
+      else as[kx * P + m] = 0.0;
+      if (pb) cp_async8(bs + kx * P + m, pb, true);
+      else bs[kx * P + m] = 0.0;
     }
   };
   __syncthreads();  // previous users of the stage buffers are done
@@ -157,13 +160,13 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       // write target: column-group tj of the same rows; the 4 column groups of a row group
       // read all of W's columns, so results go to the Yws-like staging slot first
       double* st = p.part + u * int64_t(32 * 32);
-      pr_tile32(
-          sm, [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.T0.ld : nullptr; },
+      pr_tile32kx(
+          sm, 128, [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.T0.ld : nullptr; },
           [&](int kk, int n) -> const double* {
             const int cc = c0 + n;
             return cc >= kk ? Di + cc + int64_t(kk) * p.dld : nullptr;  // D^{-T}(kk, cc) = Dinv(cc, kk)
           },
-          [&](int m, int n, double v) { __stcg(st + m + n * 32, v); });
+          [&](int m, int n, double v) { __stcg(st + m + n * 32, v); }, [](int) { return true; }, [](int) { return true; });
     }
     __threadfence();
     cg::this_grid().sync();
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       const int a0 = 32 * ti, c0 = 32 * tj;
       double* slot = p.part + bk * int64_t(128 * 128);
       // kk < 128 -> Rdot(a, kk) R(c, kk); kk >= 128 -> R(a, kk') Rdot(c, kk')
-      pr_tile32k(
+      pr_tile32kx(
           sm, p.single ? 128 : 256,
           [&](int m, int kk) -> const double* {
             const int a = a0 + m;
@@ -302,7 +305,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
           [&](int m, int n, double v) {
             const int a = a0 + m, cc = c0 + n;
             if (a >= cc) __stcg(slot + a + cc * 128, v);
-          });
+          },
+          [](int) { return true; }, [](int) { return true; });  // rows of Rdot / R (A) and of R / Rdot (B): contiguous along m / n
     }
   }
   __threadfence();
@@ -367,8 +371,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
     const double* Ab = optr<double>(p.A, b) + p.j + int64_t(p.j) * p.A.ld;
     double* Yb = p.Yws + b * 128 * 128;
     const int a0 = 32 * ti, c0 = 32 * tj;
-    pr_tile32(
-        sm,
+    pr_tile32kx(
+        sm, 128,
         [&](int m, int k) -> const double* {  // A(m, k) = Dinv(a0 + m, k)
           const int a = a0 + m;
           return (k < w && a < w && k <= a) ? Di + a + int64_t(k) * p.dld : nullptr;
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
           if (k >= w || cc >= w) return nullptr;
           return k >= cc ? Ab + k + int64_t(cc) * p.A.ld : Ab + cc + int64_t(k) * p.A.ld;
         },
-        [&](int m, int n, double v) { Yb[(a0 + m) + (c0 + n) * 128] = v; });
+        [&](int m, int n, double v) { Yb[(a0 + m) + (c0 + n) * 128] = v; }, [](int) { return true; }, [](int) { return false; });
   }
   __threadfence();
   cg::this_grid().sync();
@@ -391,8 +395,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
     const double* Yb = p.Yws + b * 128 * 128;
     double* Fb = p.Fws + b * 128 * 128;
     const int a0 = 32 * ti, c0 = 32 * tj;
-    pr_tile32(
-        sm,
+    pr_tile32kx(
+        sm, 128,
         [&](int m, int k) -> const double* { return (k < w && a0 + m < w) ? Yb + (a0 + m) + k * 128 : nullptr; },
         [&](int k, int n) -> const double* {  // B(k, n) = Dinv(c0 + n, k)
           const int cc = c0 + n;
@@ -401,7 +405,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
         [&](int m, int n, double v) {
           const int a = a0 + m, cc = c0 + n;
           Fb[a + cc * 128] = a > cc ? v : (a == cc ? 0.5 * v : 0.0);
-        });
+        },
+        [](int) { return true; }, [](int) { return true; });
   }
   __threadfence();
   cg::this_grid().sync();
@@ -418,8 +423,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
       for (int e = tid; e < 32 * 32; e += PR_THREADS) Dcb[(a0 + (e & 31)) + (c0 + (e >> 5)) * 132] = 0.0;
       continue;
     }
-    pr_tile32(
-        sm,
+    pr_tile32kx(
+        sm, 128,
         [&](int m, int k) -> const double* {  // A(m, k) = D(a0 + m, k)
           const int a = a0 + m;
           return (k < w && a < w && k <= a) ? Lb + a + int64_t(k) * p.L.ld : nullptr;
@@ -433,7 +438,8 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
           const bool low = a >= cc && a < w && cc < w;
           if (low) Ab[a + int64_t(cc) * p.A.ld] = v;
           Dcb[a + cc * 132] = low ? v : 0.0;
-        });
+        },
+        [](int) { return true; }, [](int) { return false; });
   }
 }
 

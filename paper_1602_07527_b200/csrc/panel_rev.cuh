@@ -68,42 +68,100 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(valid ? 8 : 0));
 }
 
-// One 32 x 32 output tile of C = A B (K = 128, or any multiple of 128 for pr_tile32k,
-// zero-padded) on a CTA.  The source functors
-// return a global pointer to A(m, k) / B(k, n), or nullptr for a zero; every element is
-// staged by an 8-byte cp.async (all in flight at once) into shared memory as As[m][k],
-// Bs[n][k] (pitch 132: conflict-free DMMA fragment loads).  Each warp owns two 8 x 8
-// sub-tiles; the epilogue functor gets (row m, column n, value).
-template <class FA, class FB, class EP>
-__device__ __forceinline__ void pr_tile32k(double* sm, int K, FA fa, FB fb, EP ep) {
-  constexpr int P = 132;
-  double* As = sm;
-  double* Bs = sm + 32 * P;
+__device__ __forceinline__ void cp_async_wait_n(int n) {  // all but the n most recent groups
+  switch (n) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    case 3: cp_async_wait<3>(); break;
+    case 4: cp_async_wait<4>(); break;
+    case 5: cp_async_wait<5>(); break;
+    case 6: cp_async_wait<6>(); break;
+    default: cp_async_wait<7>(); break;
+  }
+}
+
+// One 32 x 32 output tile of C = A B (K any multiple of 128, zero-padded) on a CTA.  The source
+// functors return a global pointer to A(m, k) / B(k, n), or nullptr for a zero; every element is
+// staged by an 8-byte cp.async into shared memory.  K advances in 128-wide chunks, two in flight
+// (double buffer), each chunk in four commit groups of 32 k, so the DMMA work on one group
+// overlaps the landing of the next.  am(kb) tells whether A is contiguous along m in the chunk
+// starting at k = kb (a column-major block): its copies then walk m (coalesced) and the chunk is
+// stored [k][m] (pitch 36); otherwise they walk k and it is stored [m][k] (pitch 132).  bn(kb)
+// likewise for B along n (stored [k][n], else [n][k]).  Each warp owns two 8 x 8 sub-tiles; the
+// epilogue functor gets (row m, column n, value).
+constexpr int PT_P = 132, PT_PKM = 36;
+constexpr int PT_A = 128 * PT_PKM > 32 * PT_P ? 128 * PT_PKM : 32 * PT_P;  // 4608 doubles
+constexpr int PT_SLOT = 2 * PT_A;                                          // A and B, 9216 doubles
+static_assert(2 * PT_SLOT * 8 <= PR_SMEM, "pr_tile32k buffers exceed the panel kernels' shared memory");
+
+template <class FA, class FB, class EP, class AM, class BN>
+__device__ __forceinline__ void pr_tile32kx(double* sm, int K, FA fa, FB fb, EP ep, AM am, BN bn) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int mt = warp >> 1, nt0 = (warp & 1) * 2;  // sub-tiles (mt, nt0) and (mt, nt0 + 1)
   double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  for (int kb = 0; kb < K; kb += 128) {
-    __syncthreads();  // smem reuse
-    for (int e = tid; e < 32 * 128; e += PR_THREADS) {
-      const int k = e & 127, m = e >> 7;
-      const double* pa = fa(m, kb + k);
-      const double* pb = fb(kb + k, m);
-      cp_async8(As + m * P + k, pa ? pa : As, pa != nullptr);
-      cp_async8(Bs + m * P + k, pb ? pb : Bs, pb != nullptr);
+  const int nch = (K + 127) / 128;
+  auto load = [&](int ch) {
+    double* As = sm + (ch & 1) * PT_SLOT;
+    double* Bs = As + PT_A;
+    const int kb = 128 * ch;
+    const bool mf = am(kb), nf = bn(kb);
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      for (int e = tid; e < 32 * 32; e += PR_THREADS) {
+        // an element with no source (nullptr) is a zero: a plain shared store (a zero-size
+        // cp.async would still need a valid global source address)
+        {
+          const int k = nf ? 32 * q + (e >> 5) : 32 * q + (e & 31), nn = nf ? (e & 31) : (e >> 5);
+          const double* pb = fb(kb + k, nn);
+          double* db = Bs + (nf ? k * PT_PKM + nn : nn * PT_P + k);
+          if (pb) cp_async8(db, pb, true);
+          else *db = 0.0;
+        }
+        {
+          const int k = mf ? 32 * q + (e >> 5) : 32 * q + (e & 31), m = mf ? (e & 31) : (e >> 5);
+          const double* pa = fa(m, kb + k);
+          double* da = As + (mf ? k * PT_PKM + m : m * PT_P + k);
+          if (pa) cp_async8(da, pa, true);
+          else *da = 0.0;
+        }
+      }
+      cp_async_commit();
     }
-    cp_async_wait_all();
-    __syncthreads();
-#pragma unroll 8
-    for (int kq = 0; kq < 32; ++kq) {
-      const double a = As[(8 * mt + g) * P + 4 * kq + t];
+  };
+  __syncthreads();  // shared memory reuse
+  load(0);
+#pragma unroll 1
+  for (int ch = 0; ch < nch; ++ch) {
+    const bool next = ch + 1 < nch;
+    if (next) load(ch + 1);
+    const double* As = sm + (ch & 1) * PT_SLOT;
+    const double* Bs = As + PT_A;
+    const bool mf = am(128 * ch), nf = bn(128 * ch);
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      cp_async_wait_n(3 - q + (next ? 4 : 0));
+      __syncthreads();
 #pragma unroll
-      for (int u = 0; u < 2; ++u) dmma884(c[u][0], c[u][1], a, Bs[(8 * (nt0 + u) + g) * P + 4 * kq + t]);
+      for (int kq = 8 * q; kq < 8 * q + 8; ++kq) {
+        const double a = mf ? As[(4 * kq + t) * PT_PKM + 8 * mt + g] : As[(8 * mt + g) * PT_P + 4 * kq + t];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          dmma884(c[u][0], c[u][1], a,
+                  nf ? Bs[(4 * kq + t) * PT_PKM + 8 * (nt0 + u) + g] : Bs[(8 * (nt0 + u) + g) * PT_P + 4 * kq + t]);
+      }
     }
+    __syncthreads();  // this buffer is refilled by chunk ch + 2
   }
 #pragma unroll
   for (int u = 0; u < 2; ++u)
 #pragma unroll
     for (int e = 0; e < 2; ++e) ep(8 * mt + g, 8 * (nt0 + u) + 2 * t + e, c[u][e]);
+}
+
+template <class FA, class FB, class EP>
+__device__ __forceinline__ void pr_tile32k(double* sm, int K, FA fa, FB fb, EP ep) {
+  pr_tile32kx(sm, K, fa, fb, ep, [](int) { return false; }, [](int) { return false; });
 }
 
 template <class FA, class FB, class EP>
@@ -139,7 +197,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
       const double* Lb = optr<double>(p.L, b) + p.k + int64_t(p.j) * p.L.ld;
       const double* Sb = p.Sall + b * p.s_stride + int64_t(p.nblk - (p.n - (p.k + rb)) / 128) * p.s_blk;
       double* Cb = optr_w<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;
-      pr_tile32k(
+      pr_tile32kx(
           sm, pk,
           [&](int m, int kk) -> const double* {  // M(r0 + m, k + kk)
             const int r = r0 + m - p.k, cblk = kk & ~127;
@@ -150,7 +208,9 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
           [&](int kk, int n) -> const double* { return c0 + n < w ? Lb + kk + int64_t(c0 + n) * p.L.ld : nullptr; },
           [&](int m, int n, double v) {
             if (c0 + n < w) Cb[m + int64_t(c0 + n) * p.A.ld] -= v;
-          });
+          },
+          [&](int kb) { return kb <= rb; },  // T(r, c) / S columns: contiguous along m
+          [](int) { return false; });
     }
     __threadfence();
     cooperative_groups::this_grid().sync();
@@ -171,13 +231,14 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
       const double* Cb = optr<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;
       const double* Di = p.Dinv + b * p.dstride;
       double* st = p.Wst + bt * (128 * 128) + 32 * ti;  // staging, ld 128
-      pr_tile32(
-          sm, [&](int m, int k) -> const double* { return k < w ? Cb + m + int64_t(k) * p.A.ld : nullptr; },
+      pr_tile32kx(
+          sm, 128, [&](int m, int k) -> const double* { return k < w ? Cb + m + int64_t(k) * p.A.ld : nullptr; },
           [&](int k, int n) -> const double* {  // D^{-1}(k, c0 + n), zero above the diagonal
             const int cc = c0 + n;
             return (k < w && cc < w && k >= cc) ? Di + k + int64_t(cc) * p.dld : nullptr;
           },
-          [&](int m, int n, double v) { __stcg(st + m + (c0 + n) * 128, v); });
+          [&](int m, int n, double v) { __stcg(st + m + (c0 + n) * 128, v); }, [](int) { return true; },
+          [](int) { return false; });
     }
     __threadfence();
     cooperative_groups::this_grid().sync();
