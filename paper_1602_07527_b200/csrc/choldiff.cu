@@ -70,6 +70,7 @@ struct ProfRec {
   cudaEvent_t a, b;
   int cls;
   double flops;
+  cudaStream_t st;
 };
 struct Prof {
   bool on = false;
@@ -240,7 +241,7 @@ struct Ctx {
   // call before a launch: opens a timing bracket when profiling is on
   void pre(int cls, double flops) {
     if (!g_prof.on) return;
-    ProfRec r{g_prof.ev(), g_prof.ev(), cls, flops};
+    ProfRec r{g_prof.ev(), g_prof.ev(), cls, flops, st};
     cudaEventRecord(r.a, st);
     g_prof.recs.push_back(r);
   }
@@ -674,15 +675,47 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
   }
 }
 
+// fp32 batches with 128-wide panels: the diagonal blocks on k_rf_diag128, the 128-wide inverses built
+// from 64-wide ones (CD_NO_DIAG128: the fp64-DMMA sweeps and inverses of width 128 instead)
+static bool g_no_diag128 = getenv("CD_NO_DIAG128") != nullptr;
+static bool diag128_route(int n, int nb, const Opnd& L) {
+  return nb == 128 && n % 128 == 0 && !L.arr && !g_no_diag128 && !g_no_hmma_diag;
+}
+
+// (cd_chol_rev_fwd, 128-wide route: the combine runs on its own stream beside the two sweeps, which
+// wait for it -- g_dinv_wait -- only before their first GEMM against D^{-1}; their diagonal-block
+// kernels read just the 64-wide diagonals)
+static thread_local cudaEvent_t g_dinv_wait = nullptr;
+static void wait_dinv(Ctx& c) {
+  if (g_dinv_wait && !c.plan && c.ok()) c.err = note_cuda(cudaStreamWaitEvent(c.st, g_dinv_wait, 0));
+}
+
 template <typename T>
-static void run_trinv(Ctx& c, int n, int nb, bool reverse, int64_t batch, Opnd L, T* Dinv) {
+static void run_trinv(Ctx& c, int n, int nb, bool reverse, int64_t batch, Opnd L, T* Dinv, bool combine = true) {
   if (c.plan || !c.ok()) return;
   const int nblk = nblocks(n, nb);
+  if (sizeof(T) == 4 && diag128_route(n, nb, L)) {
+    // the 64-wide inverses straight onto the diagonals of the 128-wide blocks, then the
+    // lower-left blocks (rf32_inv128)
+    const size_t smem = dmma_cta_smem(8);
+    set_smem(k_trinv_dmma<T>, smem);
+    c.pre(CD_PROF_TRINV, 0.0);
+    k_trinv_dmma<T><<<dim3(n / 64, unsigned(batch)), DC_THREADS, smem, c.st>>>(n, 64, reverse ? 1 : 0, L, Dinv, 128,
+                                                                             int64_t(64) * 128, 64);
+    c.launched();
+    if (!combine) return;
+    c.pre(CD_PROF_TRINV, 0.0);
+    c.err = note_cuda(rf32_inv128(n, batch, reinterpret_cast<const float*>(static_cast<const T*>(L.base) + L.off), L.ld,
+                                  L.stride, reinterpret_cast<float*>(Dinv), c.st));
+    ++g_launches;
+    if (g_prof.on && !g_prof.recs.empty()) cudaEventRecord(g_prof.recs.back().b, c.st);
+    return;
+  }
   const size_t smem = dmma_cta_smem((nb + 7) / 8);
   set_smem(k_trinv_dmma<T>, smem);
   c.pre(CD_PROF_TRINV, 0.0);
   k_trinv_dmma<T><<<dim3(nblk, unsigned(batch)), DC_THREADS, smem, c.st>>>(n, nb, reverse ? 1 : 0, L, Dinv, nb,
-                                                                          int64_t(nb) * nb);
+                                                                          int64_t(nb) * nb, 0);
   c.launched();
 }
 
@@ -701,6 +734,19 @@ static void diag_block(Ctx& c, bool rev, int w, int64_t batch, Opnd L, Opnd A, O
                                     static_cast<const float*>(Dinv_q.base) + Dinv_q.off, Dinv_q.stride,
                                     S.base ? const_cast<float*>(static_cast<const float*>(S.base)) + S.off : nullptr,
                                     S.ld, S.stride, c.st));
+      ++g_launches;
+      if (g_prof.on && !g_prof.recs.empty()) cudaEventRecord(g_prof.recs.back().b, c.st);
+      return;
+    }
+    if (w == 128 && !L.arr && !A.arr && !S.arr && !Dinv_q.arr && Dinv_q.ld == 128 && !g_no_diag128 && !g_no_hmma_diag) {
+      if (c.plan || !c.ok()) return;
+      c.pre(CD_PROF_SWEEP, double(batch) * (rev ? (4.0 * w * w * w + 3.0 * w * w + 11.0 * w) / 6
+                                                : (4.0 * w * w * w + 3.0 * w * w + 5.0 * w) / 6));
+      c.err = note_cuda(rf32_diag128(rev, batch, static_cast<const float*>(L.base) + L.off, L.ld, L.stride,
+                                     const_cast<float*>(static_cast<const float*>(A.base)) + A.off, A.ld, A.stride,
+                                     static_cast<const float*>(Dinv_q.base) + Dinv_q.off, Dinv_q.ld, Dinv_q.stride,
+                                     S.base ? const_cast<float*>(static_cast<const float*>(S.base)) + S.off : nullptr,
+                                     S.ld, S.stride, c.st));
       ++g_launches;
       if (g_prof.on && !g_prof.recs.empty()) cudaEventRecord(g_prof.recs.back().b, c.st);
       return;
@@ -781,6 +827,7 @@ static void blocked_rev(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
     const Opnd W = w_inplace ? Cbar : ws_opnd(Wws, int64_t(n) * nb, std::max(p, 1));
     if (p > 0) {
       // Cbar <- Cbar D^{-1}
+      if (qb == nblk - 2) wait_dinv(c);
       Gemm<T>(c, p, w, 0, 0, batch)
           .seg(Cbar, Dinv_q, w)
           .flops(double(p) * w * (w + 1))  // TRSM  Cbar D^{-1}
@@ -1183,6 +1230,7 @@ static void blocked_fwd(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A, in
       if (q > 0) g.seg(sub(A, k, 0), sub(L, j, 0), q).seg(sub(L, k, 0), sub(A, j, 0), q);
       g.seg(sub(L, k, j), Dc, w);
       g.run(sub(A, k, j), W, -1.0, 1.0, 0, part_ws);
+      if (qb == 0) wait_dinv(c);
       Gemm<T>(c, p, w, 0, 1, batch)
           .seg(W, Dinv_q, w)
           .flops(double(p) * w * (w + 1))  // TRSM  X D^{-T}
@@ -1542,11 +1590,14 @@ struct Call {
   int* info;
 };
 
-static int default_nb(cd_dtype dt, int64_t n) {
-  // fp64: 128 (the left-looking schedule's tile).  fp32 mid-size (batched tf32 path):
-  // 64 -- the on-chip diagonal-block kernels then fit several CTAs per SM, which beats
-  // the extra GEMM launches (1024 x 512 batched: rev 4.28 -> 3.39 ms, fwd 4.10 -> 2.83 ms)
-  if (dt == CD_F32 && n <= 1024) return 64;
+static int default_nb(cd_dtype dt, int64_t n, int64_t batch, bool arr) {
+  // fp64: 128 (the left-looking schedule's tile).  fp32 mid-size (batched tf32 path): 128 for
+  // strided batches with n % 128 == 0 -- the trailing updates are memory-bound and their traffic
+  // falls with the panel count, the 128-wide diagonal blocks run on k_rf_diag128 (configs[3]
+  // rev + fwd 3.54 -> 2.93 ms); otherwise 64, whose on-chip diagonal-block kernels fit several
+  // CTAs per SM (round 1, with the fp64-DMMA 128-wide sweeps: rev 4.28 -> 3.39 ms, fwd 4.10 -> 2.83 ms)
+  if (dt == CD_F32 && n <= 1024)
+    return (batch > 1 && n % 128 == 0 && !arr && !g_no_diag128 && !g_no_hmma_diag) ? 128 : 64;
   return 128;
 }
 
@@ -1733,7 +1784,7 @@ static void drive_layered(Ctx& c, const Call& k) {
     run_sweep_small<T>(c, k.op == CD_OP_REV, n, k.batch, k.L, k.A, k.o.out_mode, null_opnd(), k.info);
     return;
   }
-  const int nb = std::min(n, k.o.nb > 0 ? k.o.nb : default_nb(k.dt, n));
+  const int nb = std::min(n, k.o.nb > 0 ? k.o.nb : default_nb(k.dt, n, k.batch, k.L.arr || k.A.arr));
   if (nb > DC_NMAX) {  // diagonal blocks must fit the on-chip sweep / inverse kernels
     c.err = CD_ERR_UNSUPPORTED;
     return;
@@ -2104,9 +2155,11 @@ int cd_chol_fwd_fused_strided_batched(cd_dtype dt, int64_t n, void* A, int64_t l
 // ---- both sweeps of one factor on two streams (cd_chol_rev_fwd_strided_batched) ----
 struct SideStream {  // per device and host thread; released at thread exit
   cudaStream_t s = nullptr;
+  cudaStream_t s2 = nullptr;  // the 128-wide inverses' completion (rf32_inv128) beside both sweeps
   std::vector<cudaEvent_t> ev;
   ~SideStream() {
     if (s) cudaStreamDestroy(s);
+    if (s2) cudaStreamDestroy(s2);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
   }
 };
@@ -2114,7 +2167,7 @@ static thread_local SideStream g_side[64];
 
 // the batched fp32 right-looking drivers share one set of diagonal-block inverses (configs[3])
 static int shared_dinv_nb(cd_dtype dt, int64_t n, int64_t batch, const cd_opts& o) {
-  const int nb = int(std::min<int64_t>(n, o.nb > 0 ? o.nb : default_nb(dt, n)));
+  const int nb = int(std::min<int64_t>(n, o.nb > 0 ? o.nb : default_nb(dt, n, batch, false)));
   const bool ok = dt == CD_F32 && batch > 1 && batch <= kGridBatch && n > DC_NMAX && nb <= DC_NMAX &&
                   n % nb == 0 && o.route != CD_ROUTE_SYMBOLIC;
   return ok ? nb : 0;
@@ -2147,7 +2200,13 @@ size_t cd_workspace_size(cd_op op, cd_dtype dt, int64_t n, int64_t batch, const 
   const cd_opts o = opts ? *opts : kDefaultOpts;
   Call k{op, dt, n, batch, null_opnd(), null_opnd(), o, nullptr};
   k.L.ld = k.A.ld = n;
-  return plan_size(k);
+  size_t need = plan_size(k);
+  if (dt == CD_F32 && o.nb == 0) {  // pointer-array batches take nb = 64 (default_nb)
+    Call k64 = k;
+    k64.o.nb = 64;
+    need = std::max(need, plan_size(k64));
+  }
+  return need;
 }
 
 size_t cd_workspace_size_rev_fwd(cd_dtype dt, int64_t n, int64_t batch, const cd_opts* opts) {
@@ -2195,12 +2254,23 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
   if (!g_side[dev].s && (r = note_cuda(cudaStreamCreateWithFlags(&g_side[dev].s, cudaStreamNonBlocking)))) return r;
   std::vector<cudaEvent_t>& evs = g_side[dev].ev;
   if (evs.empty()) {
-    evs.resize(2);
+    evs.resize(4);
     for (auto& e : evs)
       if ((r = note_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)))) return r;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream), side = g_side[dev].s;
   const int snb = shared_dinv_nb(dt, n, batch, o);
+  const Opnd Lop{L, nullptr, strideL, ldl, 0};
+  const bool split_inv = snb && dt == CD_F32 && diag128_route(int(n), snb, Lop);
+  if (split_inv && !g_side[dev].s2 && (r = note_cuda(cudaStreamCreateWithFlags(&g_side[dev].s2, cudaStreamNonBlocking))))
+    return r;
+  struct ExtReset {  // the shared-inverse hand-over is scoped to this call, error returns included
+    ~ExtReset() {
+      g_ext_dinv = nullptr;
+      g_ext_dinv_nb = 0;
+      g_dinv_wait = nullptr;
+    }
+  } ext_reset;
   if (snb) {  // the inverses of the shared factor, once, before the two sweeps fork
     Ctx c;
     c.plan = false;
@@ -2208,8 +2278,21 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
     c.st = st;
     c.sms = sm_count();
     float* Dinv = reinterpret_cast<float*>(static_cast<char*>(ws) + ws_dinv);
-    run_trinv<float>(c, int(n), snb, false, batch, Opnd{L, nullptr, strideL, ldl, 0}, Dinv);
+    run_trinv<float>(c, int(n), snb, false, batch, Lop, Dinv, !split_inv);
     if (c.err) return c.err;
+    if (split_inv) {  // the 128-wide completion on s2, awaited by the sweeps' first D^{-1} GEMMs
+      if ((r = note_cuda(cudaEventRecord(evs[2], st)))) return r;
+      if ((r = note_cuda(cudaStreamWaitEvent(g_side[dev].s2, evs[2], 0)))) return r;
+      Ctx c2 = c;
+      c2.st = g_side[dev].s2;
+      c2.pre(CD_PROF_TRINV, 0.0);
+      c2.err = note_cuda(rf32_inv128(int(n), batch, static_cast<const float*>(L), ldl, strideL, Dinv, c2.st));
+      ++g_launches;
+      if (g_prof.on && !g_prof.recs.empty()) cudaEventRecord(g_prof.recs.back().b, c2.st);
+      if (c2.err) return c2.err;
+      if ((r = note_cuda(cudaEventRecord(evs[3], g_side[dev].s2)))) return r;
+      g_dinv_wait = evs[3];
+    }
     g_ext_dinv = Dinv;
     g_ext_dinv_nb = snb;
   }
@@ -2225,8 +2308,10 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
   const int rf = execute(kf, static_cast<char*>(ws) + ws_rev, ws_dinv - ws_rev, side, 14);
   g_ext_dinv = nullptr;
   g_ext_dinv_nb = 0;
+  g_dinv_wait = nullptr;
   const int rj = note_cuda(cudaEventRecord(evs[1], side));
   const int rw = rj ? rj : note_cuda(cudaStreamWaitEvent(st, evs[1], 0));
+  // (`stream` also ends after s2's combine: the sweeps waited for it)
   return r ? r : (rf ? rf : rw);
 }
 
@@ -2439,13 +2524,22 @@ void cd_profile_reset(void) {
 int cd_profile_read(int cls, double* ms, double* flops, int64_t* launches) {
   double t = 0.0, f = 0.0;
   int64_t cnt = 0;
+  // CD_PROF_DUMP (measurement switch): list every recorded launch on stderr, in order
+  static const bool dump = getenv("CD_PROF_DUMP") != nullptr;
   for (const ProfRec& r : g_prof.recs) {
-    if (r.cls != cls) continue;
+    if (r.cls != cls && !(dump && cls == 0)) continue;
     cudaError_t e = cudaEventSynchronize(r.b);
     if (e != cudaSuccess) return note_cuda(e);
     float x = 0.f;
     e = cudaEventElapsedTime(&x, r.a, r.b);
     if (e != cudaSuccess) return note_cuda(e);
+    if (dump && cls == 0) {
+      float t0 = 0.f;
+      cudaEventElapsedTime(&t0, g_prof.recs[0].a, r.a);
+      fprintf(stderr, "prof cls %d  %9.1f us  %.3g flop   [start %8.1f us, stream %p]\n", r.cls, 1e3 * x, r.flops,
+              1e3 * t0, static_cast<void*>(r.st));
+    }
+    if (r.cls != cls) continue;
     t += x;
     f += r.flops;
     ++cnt;

@@ -719,12 +719,50 @@ struct Diag64 {
   int64_t ldl, sL;
   float* A;
   int64_t lda, sA;
-  const float* Dinv;  // 64 x 64 blocks, ld 64, batch stride dstride
+  const float* Dinv;  // 64 x 64 blocks, ld 64 (128 x 128, ld ldi, for k_rf_diag128), batch stride dstride
   int64_t dstride;
   float* S;
   int64_t lds, sS;
   int rev;
+  int64_t ldi;
 };
+// Eq. 10 on one 64 x 64 block: D in bD, D^{-1} in bDi, Dbar' (lower, zeros above) in bIn; scratch
+// bT (P, then X1) and bU (Psym).  out(i, j, v) receives every element of the symmetric
+// X = D^{-T} (P + P^T) D^{-1}, P = Phi(D^T Dbar'); the result is Dbar = Phi(X), S = Phi(X) + Phi(X)^T
+template <class F>
+__device__ __forceinline__ void eq10_64(int pw, int pt, uint32_t bD, uint32_t bDi, uint32_t bIn, uint32_t bT,
+                                        uint32_t bU, F out) {
+  gemm64(pw, rowmajor(bD).tr(), rowmajor(bIn), [&](int r, int c, float v) { sts(el(bT, r, c), v); });  // P
+  panel_sync();
+  for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Psym
+    const int i = e >> 6, j = e & 63;
+    sts(el(bU, i, j), i >= j ? lds(el(bT, i, j)) : lds(el(bT, j, i)));
+  }
+  panel_sync();
+  gemm64(pw, rowmajor(bDi).tr(), rowmajor(bU), [&](int r, int c, float v) { sts(el(bT, r, c), v); });  // X1
+  panel_sync();
+  gemm64(pw, rowmajor(bT), rowmajor(bDi), out);  // X
+}
+
+// Eq. 8 on one 64 x 64 block: D in bD, D^{-1} in bDi, Ddot' (lower) in bIn; scratch bT; bIn is
+// overwritten.  out(r, c, v) receives every element of Ddot = D Phi(D^{-1} Ddot'_sym D^{-T})
+// (lower triangular: zero above the diagonal)
+template <class F>
+__device__ __forceinline__ void eq8_64(int pw, int pt, uint32_t bD, uint32_t bDi, uint32_t bIn, uint32_t bT, F out) {
+  for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Ddot'_sym
+    const int i = e >> 6, c = e & 63;
+    sts(el(bT, i, c), i >= c ? lds(el(bIn, i, c)) : lds(el(bIn, c, i)));
+  }
+  panel_sync();
+  gemm64(pw, rowmajor(bDi), rowmajor(bT), [&](int r, int c, float v) { sts(el(bIn, r, c), v); });  // Y
+  panel_sync();
+  gemm64(pw, rowmajor(bIn), rowmajor(bDi).tr(), [&](int r, int c, float v) {  // Z = Phi(Y D^{-T})
+    sts(el(bT, r, c), (r > c) ? v : (r == c ? 0.5f * v : 0.f));
+  });
+  panel_sync();
+  gemm64(pw, rowmajor(bD), rowmajor(bT), out);  // Ddot = D Z
+}
+
 __global__ void __launch_bounds__(PANEL_THREADS) k_rf_diag64(const Diag64 q) {
   extern __shared__ __align__(16) unsigned char smem_d64[];
   const uint32_t b0 = smem_u32(smem_d64), b1 = b0 + 4 * SCR, b2 = b1 + 4 * SCR, b3 = b2 + 4 * SCR, b4 = b3 + 4 * SCR;
@@ -744,16 +782,7 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_rf_diag64(const Diag64 q) {
   }
   panel_sync();
   if (q.rev) {
-    gemm64(pw, rowmajor(b1).tr(), rowmajor(b0), [&](int r, int c, float v) { sts(el(b3, r, c), v); });  // P
-    panel_sync();
-    for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Psym
-      const int i = e >> 6, j = e & 63;
-      sts(el(b4, i, j), i >= j ? lds(el(b3, i, j)) : lds(el(b3, j, i)));
-    }
-    panel_sync();
-    gemm64(pw, rowmajor(b2).tr(), rowmajor(b4), [&](int r, int c, float v) { sts(el(b3, r, c), v); });  // X1
-    panel_sync();
-    gemm64(pw, rowmajor(b3), rowmajor(b2), [&](int i, int j, float v) {  // X
+    eq10_64(pw, pt, b1, b2, b0, b3, b4, [&](int i, int j, float v) {
       if (i > j) {
         A[i + int64_t(j) * q.lda] = v;
         if (S) {
@@ -766,22 +795,243 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_rf_diag64(const Diag64 q) {
       }
     });
   } else {
-    for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Ddot'_sym
-      const int i = e >> 6, c = e & 63;
-      sts(el(b3, i, c), i >= c ? lds(el(b0, i, c)) : lds(el(b0, c, i)));
-    }
-    panel_sync();
-    gemm64(pw, rowmajor(b2), rowmajor(b3), [&](int r, int c, float v) { sts(el(b0, r, c), v); });  // Y
-    panel_sync();
-    gemm64(pw, rowmajor(b0), rowmajor(b2).tr(), [&](int r, int c, float v) {  // Z = Phi(Y D^{-T})
-      sts(el(b3, r, c), (r > c) ? v : (r == c ? 0.5f * v : 0.f));
-    });
-    panel_sync();
-    gemm64(pw, rowmajor(b1), rowmajor(b3), [&](int r, int c, float v) {  // Ddot = D Z
+    eq8_64(pw, pt, b1, b2, b0, b3, [&](int r, int c, float v) {
       if (r >= c) A[r + int64_t(c) * q.lda] = v;
       if (S) S[r + int64_t(c) * q.lds] = r >= c ? v : 0.f;
     });
   }
+}
+
+// 64 x 64 x 128 product over the 8 panel warps: A1 B1 + A2 B2 (same warp layout as gemm64)
+template <class FOUT>
+__device__ __forceinline__ void gemm64x2(int pw, const SV& A1, const SV& B1, const SV& A2, const SV& B2, FOUT out) {
+  const int r0 = 16 * (pw >> 1), c0 = 32 * (pw & 1);
+  float acc[4][4];
+  zero(acc);
+  warp_mma<4>(acc, NBK, A1.sub(r0, 0), B1.sub(0, c0));
+  warp_mma<4>(acc, NBK, A2.sub(r0, 0), B2.sub(0, c0));
+  for_acc(acc, [&](int r, int c, float v) { out(r0 + r, c0 + c, v); });
+}
+
+// ---------------------------------------------------------------- 128-wide diagonal blocks of the
+// layered fp32 schedule (N_b = 128 for the trailing updates): the 128 x 128 block's own sweep as
+// the blocked algorithm with two 64-wide steps (PAPER.md:689-701 / 655-666 on the block), every
+// product on mma.sync from shared memory, one CTA of 256 threads per matrix.  With the block
+// [D11 0; L21 D22], inverses D11^{-1}, D22^{-1} (the diagonal blocks of the 128-wide inverse):
+//   rev:  Dbar22 = Eq10(D22, Dbar22');  Dbar21 -= S22 L21  (S22 = Dbar22 + Dbar22^T);
+//         Cbar = Dbar21 D11^{-1};  Dbar11' -= tril(Cbar^T L21);  Dbar11 = Eq10(D11, Dbar11')
+//         S (128 x 128, dense) = Dbar + Dbar^T = [S11 Cbar^T; Cbar S22]
+//   fwd:  Ddot11 = Eq8(D11, Ddot11');  Ddot21 = (Ddot21' - L21 tril(Ddot11)^T) D11^{-T};
+//         Ddot22' -= tril(Ddot21 L21^T + L21 Ddot21^T);  Ddot22 = Eq8(D22, Ddot22')
+//         S (128 x 128) = tril(Ddot), zeros above
+// Six 64 x 64 buffers (104 KB): two CTAs per SM.  The next step's operands are prefetched into
+// registers while the current step's products run.
+__global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q) {
+  extern __shared__ __align__(16) unsigned char smem_d128[];
+  const uint32_t B0 = smem_u32(smem_d128), B1 = B0 + 4 * SCR, B2 = B1 + 4 * SCR, B3 = B2 + 4 * SCR,
+                 B4 = B3 + 4 * SCR, B5 = B4 + 4 * SCR;
+  const int pt = threadIdx.x, pw = pt >> 5;
+  const int64_t b = blockIdx.x;
+  const float* L = q.L + b * q.sL;
+  float* A = q.A + b * q.sA;
+  float* S = q.S ? q.S + b * q.sS : nullptr;
+  const float* Di = q.Dinv + b * q.dstride;  // 128 x 128, ld q.ldi
+  const int64_t ldl = q.ldl, lda = q.lda, lds_ = q.lds, ldi = q.ldi;
+  const float* D11 = L;
+  const float* L21 = L + 64;
+  const float* D22 = L + 64 + 64 * ldl;
+  const float* Di11 = Di;
+  const float* Di22 = Di + 64 + 64 * ldi;
+  float* A11 = A;
+  float* A21 = A + 64;
+  float* A22 = A + 64 + 64 * lda;
+  if (q.rev) {
+    {
+      Tile64 t0, t1, t2;
+      t0.load(D22, ldl, pt, true);
+      t1.load(Di22, ldi, pt, false);
+      t2.load(A22, lda, pt, true);
+      t0.store(B1, pt);
+      t1.store(B2, pt);
+      t2.store(B0, pt);
+    }
+    Tile64 p0, p1;
+    p0.load(L21, ldl, pt, false);
+    p1.load(A21, lda, pt, false);
+    panel_sync();
+    eq10_64(pw, pt, B1, B2, B0, B3, B4, [&](int i, int j, float v) {  // Dbar22, S22
+      if (i >= j) {
+        A22[i + int64_t(j) * lda] = i == j ? 0.5f * v : v;
+        sts(el(B5, i, j), v);
+        sts(el(B5, j, i), v);
+        if (S) {
+          S[64 + i + (64 + j) * lds_] = v;
+          S[64 + j + (64 + i) * lds_] = v;
+        }
+      }
+    });
+    panel_sync();
+    p0.store(B1, pt);  // L21
+    p1.store(B0, pt);  // Dbar21'
+    Tile64 q0, q1, q2;
+    q0.load(Di11, ldi, pt, false);
+    q1.load(D11, ldl, pt, true);
+    q2.load(A11, lda, pt, true);
+    panel_sync();
+    gemm64(pw, rowmajor(B5), rowmajor(B1), [&](int r, int c, float v) {  // Dbar21 -= S22 L21
+      sts(el(B0, r, c), lds(el(B0, r, c)) - v);
+    });
+    q0.store(B2, pt);  // D11^{-1} (B2 is not read by that product)
+    panel_sync();
+    q1.store(B5, pt);  // D11 (S22 consumed)
+    gemm64(pw, rowmajor(B0), rowmajor(B2), [&](int r, int c, float v) {  // Cbar = Dbar21 D11^{-1}
+      sts(el(B3, r, c), v);
+      A21[r + int64_t(c) * lda] = v;
+      if (S) {
+        S[64 + r + int64_t(c) * lds_] = v;
+        S[c + int64_t(64 + r) * lds_] = v;
+      }
+    });
+    q2.store(B4, pt);  // Dbar11'
+    panel_sync();
+    gemm64(pw, rowmajor(B3).tr(), rowmajor(B1), [&](int r, int c, float v) {  // Dbar11' -= tril(Cbar^T L21)
+      if (r >= c) sts(el(B4, r, c), lds(el(B4, r, c)) - v);
+    });
+    panel_sync();
+    eq10_64(pw, pt, B5, B2, B4, B0, B1, [&](int i, int j, float v) {  // Dbar11, S11
+      if (i >= j) {
+        A11[i + int64_t(j) * lda] = i == j ? 0.5f * v : v;
+        if (S) {
+          S[i + int64_t(j) * lds_] = v;
+          S[j + int64_t(i) * lds_] = v;
+        }
+      }
+    });
+  } else {
+    {
+      Tile64 t0, t1, t2;
+      t0.load(D11, ldl, pt, true);
+      t1.load(Di11, ldi, pt, false);
+      t2.load(A11, lda, pt, true);
+      t0.store(B1, pt);
+      t1.store(B2, pt);
+      t2.store(B0, pt);
+    }
+    Tile64 p0, p1;
+    p0.load(L21, ldl, pt, false);
+    p1.load(A21, lda, pt, false);
+    panel_sync();
+    eq8_64(pw, pt, B1, B2, B0, B3, [&](int r, int c, float v) {  // Ddot11; tril copy in B4
+      const float t = r >= c ? v : 0.f;
+      if (r >= c) A11[r + int64_t(c) * lda] = v;
+      sts(el(B4, r, c), t);
+      if (S) {
+        S[r + int64_t(c) * lds_] = t;
+        S[r + int64_t(64 + c) * lds_] = 0.f;
+      }
+    });
+    panel_sync();
+    p0.store(B5, pt);  // L21
+    p1.store(B0, pt);  // Ddot21'
+    Tile64 q0, q1, q2;
+    q0.load(Di22, ldi, pt, false);
+    q1.load(D22, ldl, pt, true);
+    q2.load(A22, lda, pt, true);
+    panel_sync();
+    gemm64(pw, rowmajor(B5), rowmajor(B4).tr(), [&](int r, int c, float v) {  // W = Ddot21' - L21 tril(Ddot11)^T
+      sts(el(B0, r, c), lds(el(B0, r, c)) - v);
+    });
+    panel_sync();
+    q2.store(B4, pt);  // Ddot22' (tril(Ddot11) consumed)
+    gemm64(pw, rowmajor(B0), rowmajor(B2).tr(), [&](int r, int c, float v) {  // Ddot21 = W D11^{-T}
+      sts(el(B3, r, c), v);
+      A21[r + int64_t(c) * lda] = v;
+      if (S) S[64 + r + int64_t(c) * lds_] = v;
+    });
+    panel_sync();
+    q1.store(B1, pt);  // D22
+    q0.store(B2, pt);  // D22^{-1}
+    gemm64x2(pw, rowmajor(B3), rowmajor(B5).tr(), rowmajor(B5), rowmajor(B3).tr(),
+             [&](int r, int c, float v) {  // Ddot22' -= tril(Ddot21 L21^T + L21 Ddot21^T)
+               if (r >= c) sts(el(B4, r, c), lds(el(B4, r, c)) - v);
+             });
+    panel_sync();
+    eq8_64(pw, pt, B1, B2, B4, B0, [&](int r, int c, float v) {  // Ddot22
+      if (r >= c) A22[r + int64_t(c) * lda] = v;
+      if (S) S[64 + r + int64_t(64 + c) * lds_] = r >= c ? v : 0.f;
+    });
+  }
+}
+
+// 3xTF32 product (fp32-faithful): a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi, hi = rna(x), lo = rna(x - hi)
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = rna(x);
+  lo = rna(x - __uint_as_float(hi));
+}
+// one warp: acc[16 x 32] += A[16 x 64] B[64 x 32] in 3xTF32
+__device__ __forceinline__ void warp_mma3(float (&acc)[4][4], const SV& A, const SV& B) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll 2
+  for (int k0 = 0; k0 < NBK; k0 += 8) {
+    uint32_t ah[4], al[4];
+    split_tf32(lds(A.at(g, k0 + t)), ah[0], al[0]);
+    split_tf32(lds(A.at(g + 8, k0 + t)), ah[1], al[1]);
+    split_tf32(lds(A.at(g, k0 + t + 4)), ah[2], al[2]);
+    split_tf32(lds(A.at(g + 8, k0 + t + 4)), ah[3], al[3]);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      uint32_t bh[2], bl[2];
+      split_tf32(lds(B.at(k0 + t, nt * 8 + g)), bh[0], bl[0]);
+      split_tf32(lds(B.at(k0 + t + 4, nt * 8 + g)), bh[1], bl[1]);
+      mma8(acc[nt], al, bh);
+      mma8(acc[nt], ah, bl);
+      mma8(acc[nt], ah, bh);
+    }
+  }
+}
+
+// The 128-wide block inverses from the 64-wide ones already on their diagonal (k_trinv_dmma with
+// odd_off): [D11 0; L21 D22]^{-1} = [D11^{-1} 0; -D22^{-1} L21 D11^{-1}  D22^{-1}], the two products
+// on mma.sync in 3xTF32 (fp32-faithful); one CTA of 256 threads per block.  Dinv: 128 x 128 blocks,
+// ld 128, nblk2 per matrix.
+__global__ void __launch_bounds__(PANEL_THREADS) k_rf_inv128(int nblk2, const float* __restrict__ L, int64_t ldl,
+                                                            int64_t sL, float* __restrict__ Dinv) {
+  extern __shared__ __align__(16) unsigned char smem_i128[];
+  const uint32_t b0 = smem_u32(smem_i128), b1 = b0 + 4 * SCR, b2 = b1 + 4 * SCR;
+  const int pt = threadIdx.x, pw = pt >> 5;
+  const int64_t blk = blockIdx.x;
+  const int64_t b = blk / nblk2;
+  const int Q = int(blk - b * nblk2);
+  float* X = Dinv + blk * (128 * 128);
+  {
+    Tile64 ta, tl;
+    ta.load(X, 128, pt, false);                                                    // D11^{-1}
+    tl.load(L + b * sL + (128 * Q + 64) + int64_t(128 * Q) * ldl, ldl, pt, false);  // L21
+    ta.store(b0, pt);
+    tl.store(b1, pt);
+  }
+  Tile64 tc;
+  tc.load(X + 64 + 64 * 128, 128, pt, false);  // D22^{-1}
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {  // upper-right block
+    const int e = pt + q * PANEL_THREADS;
+    X[(e & 63) + ((e >> 6) + 64) * 128] = 0.f;
+  }
+  panel_sync();
+  const int r0 = 16 * (pw >> 1), c0 = 32 * (pw & 1);
+  {
+    float acc[4][4];
+    zero(acc);
+    warp_mma3(acc, rowmajor(b1).sub(r0, 0), rowmajor(b0).sub(0, c0));  // T = L21 D11^{-1}
+    tc.store(b2, pt);
+    panel_sync();
+    for_acc(acc, [&](int r, int c, float v) { sts(el(b1, r0 + r, c0 + c), v); });
+  }
+  panel_sync();
+  float acc[4][4];
+  zero(acc);
+  warp_mma3(acc, rowmajor(b2).sub(r0, 0), rowmajor(b1).sub(0, c0));  // D22^{-1} T
+  for_acc(acc, [&](int r, int c, float v) { X[64 + r0 + r + (c0 + c) * 128] = -v; });
 }
 
 // Block inverses D_J^{-1} (fp32 forward substitution, one CTA of 64 threads per 64 x 64 block;
@@ -948,7 +1198,7 @@ cudaError_t rf32_diag64(bool rev, int64_t batch, const float* L, int64_t ldl, in
                         int64_t sA, const float* Dinv, int64_t dstride, float* S, int64_t lds, int64_t sS,
                         cudaStream_t st) {
   using namespace rf;
-  Diag64 q{L, ldl, sL, A, lda, sA, Dinv, dstride, S, lds, sS, rev ? 1 : 0};
+  Diag64 q{L, ldl, sL, A, lda, sA, Dinv, dstride, S, lds, sS, rev ? 1 : 0, NBK};
   constexpr size_t smem = 5 * SCR * 4;
   static bool attr = false;
   if (!attr) {
@@ -956,6 +1206,33 @@ cudaError_t rf32_diag64(bool rev, int64_t batch, const float* L, int64_t ldl, in
     attr = true;
   }
   k_rf_diag64<<<unsigned(batch), PANEL_THREADS, smem, st>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t rf32_diag128(bool rev, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* A, int64_t lda,
+                         int64_t sA, const float* Dinv, int64_t ldi, int64_t dstride, float* S, int64_t lds,
+                         int64_t sS, cudaStream_t st) {
+  using namespace rf;
+  Diag64 q{L, ldl, sL, A, lda, sA, Dinv, dstride, S, lds, sS, rev ? 1 : 0, ldi};
+  constexpr size_t smem = 6 * SCR * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rf_diag128, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  k_rf_diag128<<<unsigned(batch), PANEL_THREADS, smem, st>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t rf32_inv128(int n, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* Dinv, cudaStream_t st) {
+  const int nblk2 = n / 128;
+  constexpr size_t smem = 3 * rf::SCR * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rf::k_rf_inv128, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  rf::k_rf_inv128<<<unsigned(batch * nblk2), rf::PANEL_THREADS, smem, st>>>(nblk2, L, ldl, sL, Dinv);
   return cudaGetLastError();
 }
 

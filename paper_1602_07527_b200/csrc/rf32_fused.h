@@ -39,4 +39,14 @@ cudaError_t rf32_diag64(bool rev, int64_t batch, const float* L, int64_t ldl, in
                         int64_t sA, const float* Dinv, int64_t dstride, float* S, int64_t lds, int64_t sS,
                         cudaStream_t st);
 
+// The same for 128-wide panels (the block's own sweep as two 64-wide steps, k_rf_diag128): Dinv
+// points at the 128 x 128 inverse of the block (ld ldi); S (optional) receives Dbar + Dbar^T (rev) /
+// tril(Ddot) with zeros above (fwd), 128 x 128.
+cudaError_t rf32_diag128(bool rev, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* A, int64_t lda,
+                         int64_t sA, const float* Dinv, int64_t ldi, int64_t dstride, float* S, int64_t lds,
+                         int64_t sS, cudaStream_t st);
+// Complete the 128-wide block inverses (128 x 128 each, ld 128, n / 128 per matrix, consecutive)
+// whose 64-wide diagonal blocks are in place: lower-left block from L, upper-right zero.
+cudaError_t rf32_inv128(int n, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* Dinv, cudaStream_t st);
+
 }  // namespace cd

@@ -426,11 +426,14 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
 }
 
 // ============================================================================ inverse
-// Dinv[b][q] = tril(L[j0:j0+w, j0:j0+w])^{-1}, dense w x w (ld = ldi), upper zero;
-// grid = (blocks, batch); block ranges as block_range (misc.cuh).
+// Dinv[b][q] = tril(L[j0:j0+w, j0:j0+w])^{-1}, dense w x w (ld = ldi), upper zero, at
+// Dinv + (b * blocks + q) * stride_blk + (q odd ? odd_off : 0); grid = (blocks, batch); block ranges
+// as block_range (misc.cuh).  (odd_off = 64 with stride_blk = 64 ldi and ldi = 128 puts the
+// 64-wide inverses on the diagonal of 128-wide blocks: rf32_inv128 fills in the rest.)
 template <typename TIO>
 __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
-    k_trinv_dmma(int n, int nb, int reverse, Opnd Ld, TIO* __restrict__ Dinv, int64_t ldi, int64_t stride_blk) {
+    k_trinv_dmma(int n, int nb, int reverse, Opnd Ld, TIO* __restrict__ Dinv, int64_t ldi, int64_t stride_blk,
+                 int64_t odd_off) {
   const int NBLK = (nb + 7) >> 3;  // tiling of the widest block; shorter blocks are padded
   const int NP = 8 * NBLK;
   const int NTILE = NBLK * (NBLK + 1) / 2;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
     }
   }
   __syncthreads();
-  TIO* X = Dinv + (int64_t(b) * gridDim.x + q) * stride_blk;
+  TIO* X = Dinv + (int64_t(b) * gridDim.x + q) * stride_blk + ((q & 1) ? odd_off : 0);
   for (int c = warp; c < w; c += DC_WARPS)
     for (int i = lane; i < w; i += 32) X[i + int64_t(c) * ldi] = TIO((i >= c) ? sX[tat(NBLK, i, c)] : 0.0);
 }
