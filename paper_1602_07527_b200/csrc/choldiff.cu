@@ -556,8 +556,11 @@ struct Gemm {
       return std::min(o, 2);  // TMEM: 2 x 256 columns per CTA
     });
     set_smem(kern, smem);
-    // persistent: a grid of (up to) occ CTAs per SM loops over the units
-    const unsigned g = unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(c.sms) * occ)));
+    // persistent: a grid of (up to) occ CTAs per SM loops over the units (CD_TC_SMS: measurement
+    // switch capping the SMs it takes)
+    static const int tc_sms = getenv("CD_TC_SMS") ? atoi(getenv("CD_TC_SMS")) : 0;
+    const int sms = tc_sms > 0 ? std::min(tc_sms, c.sms) : c.sms;
+    const unsigned g = unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(sms) * occ)));
     kern<<<g, tcp_threads(EPI), smem, c.st>>>(p, tm, em);
     c.launched();
     return true;

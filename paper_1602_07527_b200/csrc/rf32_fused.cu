@@ -143,26 +143,28 @@ __device__ __forceinline__ void frag_load(Frag<NT>& f, const SV& A, const SV& B,
     f.b[nt][1] = lds(B.at(k0 + t + 4, nt * 8 + g));
   }
 }
-template <int NT>
+// PRE: the operands in shared memory are already tf32-rounded (cvt.rna at store), no conversion here
+template <int NT, bool PRE = false>
 __device__ __forceinline__ void frag_mma(float (&acc)[NT][4], const Frag<NT>& f) {
-  const uint32_t a[4] = {rna(f.a[0]), rna(f.a[1]), rna(f.a[2]), rna(f.a[3])};
+  auto cv = [](float x) { return PRE ? __float_as_uint(x) : rna(x); };
+  const uint32_t a[4] = {cv(f.a[0]), cv(f.a[1]), cv(f.a[2]), cv(f.a[3])};
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const uint32_t b[2] = {rna(f.b[nt][0]), rna(f.b[nt][1])};
+    const uint32_t b[2] = {cv(f.b[nt][0]), cv(f.b[nt][1])};
     mma8(acc[nt], a, b);
   }
 }
 // one warp: acc[16 x 8 NT] += A[16 x K] B[K x 8 NT], both in shared memory (K a multiple of 16);
 // the next k-step's fragments are loaded while the current one multiplies
-template <int NT>
+template <int NT, bool PRE = false>
 __device__ __forceinline__ void warp_mma(float (&acc)[NT][4], int K, const SV& A, const SV& B) {
   Frag<NT> f0, f1;
   frag_load(f0, A, B, 0);
   for (int k0 = 0; k0 < K; k0 += 16) {
     frag_load(f1, A, B, k0 + 8);
-    frag_mma(acc, f0);
+    frag_mma<NT, PRE>(acc, f0);
     if (k0 + 16 < K) frag_load(f0, A, B, k0 + 16);
-    frag_mma(acc, f1);
+    frag_mma<NT, PRE>(acc, f1);
   }
 }
 template <int NT>
@@ -188,12 +190,12 @@ __device__ __forceinline__ void panel_sync() {  // warps 2..9
 }
 
 // 64 x 64 x 64 product over the 8 panel warps: warp pw computes rows 16 (pw>>1), columns 32 (pw&1)
-template <class FOUT>
+template <bool PRE = false, class FOUT>
 __device__ __forceinline__ void gemm64(int pw, const SV& A, const SV& B, FOUT out) {
   const int r0 = 16 * (pw >> 1), c0 = 32 * (pw & 1);
   float acc[4][4];
   zero(acc);
-  warp_mma<4>(acc, NBK, A.sub(r0, 0), B.sub(0, c0));
+  warp_mma<4, PRE>(acc, NBK, A.sub(r0, 0), B.sub(0, c0));
   for_acc(acc, [&](int r, int c, float v) { out(r0 + r, c0 + c, v); });
 }
 
@@ -209,11 +211,11 @@ struct Tile64 {
       v[q] = (!tril || i >= c) ? __ldcg(src + i + int64_t(c) * ld) : 0.f;
     }
   }
-  __device__ __forceinline__ void store(uint32_t buf, int pt) const {
+  __device__ __forceinline__ void store(uint32_t buf, int pt, bool round = false) const {
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int e = pt + q * PANEL_THREADS, i = e & 63, c = e >> 6;
-      sts(el(buf, i, c), v[q]);
+      sts(el(buf, i, c), round ? rnd(v[q]) : v[q]);
     }
   }
 };
@@ -726,41 +728,42 @@ struct Diag64 {
   int rev;
   int64_t ldi;
 };
-// Eq. 10 on one 64 x 64 block: D in bD, D^{-1} in bDi, Dbar' (lower, zeros above) in bIn; scratch
-// bT (P, then X1) and bU (Psym).  out(i, j, v) receives every element of the symmetric
-// X = D^{-T} (P + P^T) D^{-1}, P = Phi(D^T Dbar'); the result is Dbar = Phi(X), S = Phi(X) + Phi(X)^T
+// Eq. 10 on one 64 x 64 block: D in bD, D^{-1} in bDi, Dbar' (lower, zeros above) in bIn -- all three
+// tf32-rounded (the products take pre-rounded operands); scratch bT (P, then X1) and bU (Psym).
+// out(i, j, v) receives every element of the symmetric X = D^{-T} (P + P^T) D^{-1},
+// P = Phi(D^T Dbar'); the result is Dbar = Phi(X), S = Phi(X) + Phi(X)^T
 template <class F>
 __device__ __forceinline__ void eq10_64(int pw, int pt, uint32_t bD, uint32_t bDi, uint32_t bIn, uint32_t bT,
                                         uint32_t bU, F out) {
-  gemm64(pw, rowmajor(bD).tr(), rowmajor(bIn), [&](int r, int c, float v) { sts(el(bT, r, c), v); });  // P
+  gemm64<true>(pw, rowmajor(bD).tr(), rowmajor(bIn), [&](int r, int c, float v) { sts(el(bT, r, c), v); });  // P
   panel_sync();
   for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Psym
     const int i = e >> 6, j = e & 63;
-    sts(el(bU, i, j), i >= j ? lds(el(bT, i, j)) : lds(el(bT, j, i)));
+    sts(el(bU, i, j), rnd(i >= j ? lds(el(bT, i, j)) : lds(el(bT, j, i))));
   }
   panel_sync();
-  gemm64(pw, rowmajor(bDi).tr(), rowmajor(bU), [&](int r, int c, float v) { sts(el(bT, r, c), v); });  // X1
+  gemm64<true>(pw, rowmajor(bDi).tr(), rowmajor(bU), [&](int r, int c, float v) { sts(el(bT, r, c), rnd(v)); });  // X1
   panel_sync();
-  gemm64(pw, rowmajor(bT), rowmajor(bDi), out);  // X
+  gemm64<true>(pw, rowmajor(bT), rowmajor(bDi), out);  // X
 }
 
-// Eq. 8 on one 64 x 64 block: D in bD, D^{-1} in bDi, Ddot' (lower) in bIn; scratch bT; bIn is
-// overwritten.  out(r, c, v) receives every element of Ddot = D Phi(D^{-1} Ddot'_sym D^{-T})
-// (lower triangular: zero above the diagonal)
+// Eq. 8 on one 64 x 64 block: D in bD, D^{-1} in bDi (both tf32-rounded), Ddot' (lower) in bIn;
+// scratch bT; bIn is overwritten.  out(r, c, v) receives every element of
+// Ddot = D Phi(D^{-1} Ddot'_sym D^{-T}) (lower triangular: zero above the diagonal)
 template <class F>
 __device__ __forceinline__ void eq8_64(int pw, int pt, uint32_t bD, uint32_t bDi, uint32_t bIn, uint32_t bT, F out) {
   for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Ddot'_sym
     const int i = e >> 6, c = e & 63;
-    sts(el(bT, i, c), i >= c ? lds(el(bIn, i, c)) : lds(el(bIn, c, i)));
+    sts(el(bT, i, c), rnd(i >= c ? lds(el(bIn, i, c)) : lds(el(bIn, c, i))));
   }
   panel_sync();
-  gemm64(pw, rowmajor(bDi), rowmajor(bT), [&](int r, int c, float v) { sts(el(bIn, r, c), v); });  // Y
+  gemm64<true>(pw, rowmajor(bDi), rowmajor(bT), [&](int r, int c, float v) { sts(el(bIn, r, c), rnd(v)); });  // Y
   panel_sync();
-  gemm64(pw, rowmajor(bIn), rowmajor(bDi).tr(), [&](int r, int c, float v) {  // Z = Phi(Y D^{-T})
-    sts(el(bT, r, c), (r > c) ? v : (r == c ? 0.5f * v : 0.f));
+  gemm64<true>(pw, rowmajor(bIn), rowmajor(bDi).tr(), [&](int r, int c, float v) {  // Z = Phi(Y D^{-T})
+    sts(el(bT, r, c), rnd((r > c) ? v : (r == c ? 0.5f * v : 0.f)));
   });
   panel_sync();
-  gemm64(pw, rowmajor(bD), rowmajor(bT), out);  // Ddot = D Z
+  gemm64<true>(pw, rowmajor(bD), rowmajor(bT), out);  // Ddot = D Z
 }
 
 __global__ void __launch_bounds__(PANEL_THREADS) k_rf_diag64(const Diag64 q) {
@@ -776,9 +779,9 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_rf_diag64(const Diag64 q) {
     td.load(L, q.ldl, pt, true);                     // D
     ti.load(q.Dinv + b * q.dstride, NBK, pt, false);  // D^{-1}
     ta.load(A, q.lda, pt, true);                     // Dbar' / Ddot' (lower)
-    td.store(b1, pt);
-    ti.store(b2, pt);
-    ta.store(b0, pt);
+    td.store(b1, pt, true);
+    ti.store(b2, pt, true);
+    ta.store(b0, pt, true);
   }
   panel_sync();
   if (q.rev) {
@@ -808,8 +811,8 @@ __device__ __forceinline__ void gemm64x2(int pw, const SV& A1, const SV& B1, con
   const int r0 = 16 * (pw >> 1), c0 = 32 * (pw & 1);
   float acc[4][4];
   zero(acc);
-  warp_mma<4>(acc, NBK, A1.sub(r0, 0), B1.sub(0, c0));
-  warp_mma<4>(acc, NBK, A2.sub(r0, 0), B2.sub(0, c0));
+  warp_mma<4, true>(acc, NBK, A1.sub(r0, 0), B1.sub(0, c0));
+  warp_mma<4, true>(acc, NBK, A2.sub(r0, 0), B2.sub(0, c0));
   for_acc(acc, [&](int r, int c, float v) { out(r0 + r, c0 + c, v); });
 }
 
@@ -851,9 +854,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q)
       t0.load(D22, ldl, pt, true);
       t1.load(Di22, ldi, pt, false);
       t2.load(A22, lda, pt, true);
-      t0.store(B1, pt);
-      t1.store(B2, pt);
-      t2.store(B0, pt);
+      t0.store(B1, pt, true);
+      t1.store(B2, pt, true);
+      t2.store(B0, pt, true);
     }
     Tile64 p0, p1;
     p0.load(L21, ldl, pt, false);
@@ -862,8 +865,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q)
     eq10_64(pw, pt, B1, B2, B0, B3, B4, [&](int i, int j, float v) {  // Dbar22, S22
       if (i >= j) {
         A22[i + int64_t(j) * lda] = i == j ? 0.5f * v : v;
-        sts(el(B5, i, j), v);
-        sts(el(B5, j, i), v);
+        sts(el(B5, i, j), rnd(v));
+        sts(el(B5, j, i), rnd(v));
         if (S) {
           S[64 + i + (64 + j) * lds_] = v;
           S[64 + j + (64 + i) * lds_] = v;
@@ -871,21 +874,22 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q)
       }
     });
     panel_sync();
-    p0.store(B1, pt);  // L21
-    p1.store(B0, pt);  // Dbar21'
-    Tile64 q0, q1, q2;
+    p0.store(B1, pt, true);  // L21
+    p1.store(B0, pt);        // Dbar21' (exact: updated below)
+    Tile64 q0;
     q0.load(Di11, ldi, pt, false);
+    panel_sync();
+    gemm64<true>(pw, rowmajor(B5), rowmajor(B1), [&](int r, int c, float v) {  // Dbar21 -= S22 L21
+      sts(el(B0, r, c), rnd(lds(el(B0, r, c)) - v));
+    });
+    q0.store(B2, pt, true);  // D11^{-1} (B2 is not read by that product)
+    Tile64 q1, q2;
     q1.load(D11, ldl, pt, true);
     q2.load(A11, lda, pt, true);
     panel_sync();
-    gemm64(pw, rowmajor(B5), rowmajor(B1), [&](int r, int c, float v) {  // Dbar21 -= S22 L21
-      sts(el(B0, r, c), lds(el(B0, r, c)) - v);
-    });
-    q0.store(B2, pt);  // D11^{-1} (B2 is not read by that product)
-    panel_sync();
-    q1.store(B5, pt);  // D11 (S22 consumed)
-    gemm64(pw, rowmajor(B0), rowmajor(B2), [&](int r, int c, float v) {  // Cbar = Dbar21 D11^{-1}
-      sts(el(B3, r, c), v);
+    q1.store(B5, pt, true);  // D11 (S22 consumed)
+    gemm64<true>(pw, rowmajor(B0), rowmajor(B2), [&](int r, int c, float v) {  // Cbar = Dbar21 D11^{-1}
+      sts(el(B3, r, c), rnd(v));
       A21[r + int64_t(c) * lda] = v;
       if (S) {
         S[64 + r + int64_t(c) * lds_] = v;
@@ -894,8 +898,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q)
     });
     q2.store(B4, pt);  // Dbar11'
     panel_sync();
-    gemm64(pw, rowmajor(B3).tr(), rowmajor(B1), [&](int r, int c, float v) {  // Dbar11' -= tril(Cbar^T L21)
-      if (r >= c) sts(el(B4, r, c), lds(el(B4, r, c)) - v);
+    gemm64<true>(pw, rowmajor(B3).tr(), rowmajor(B1), [&](int r, int c, float v) {  // Dbar11' -= tril(Cbar^T L21)
+      if (r >= c) sts(el(B4, r, c), rnd(lds(el(B4, r, c)) - v));
     });
     panel_sync();
     eq10_64(pw, pt, B5, B2, B4, B0, B1, [&](int i, int j, float v) {  // Dbar11, S11
@@ -913,8 +917,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q)
       t0.load(D11, ldl, pt, true);
       t1.load(Di11, ldi, pt, false);
       t2.load(A11, lda, pt, true);
-      t0.store(B1, pt);
-      t1.store(B2, pt);
+      t0.store(B1, pt, true);
+      t1.store(B2, pt, true);
       t2.store(B0, pt);
     }
     Tile64 p0, p1;
@@ -924,33 +928,34 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q)
     eq8_64(pw, pt, B1, B2, B0, B3, [&](int r, int c, float v) {  // Ddot11; tril copy in B4
       const float t = r >= c ? v : 0.f;
       if (r >= c) A11[r + int64_t(c) * lda] = v;
-      sts(el(B4, r, c), t);
+      sts(el(B4, r, c), rnd(t));
       if (S) {
         S[r + int64_t(c) * lds_] = t;
         S[r + int64_t(64 + c) * lds_] = 0.f;
       }
     });
     panel_sync();
-    p0.store(B5, pt);  // L21
-    p1.store(B0, pt);  // Ddot21'
-    Tile64 q0, q1, q2;
-    q0.load(Di22, ldi, pt, false);
-    q1.load(D22, ldl, pt, true);
+    p0.store(B5, pt, true);  // L21
+    p1.store(B0, pt);        // Ddot21' (exact: updated below)
+    Tile64 q2;
     q2.load(A22, lda, pt, true);
     panel_sync();
-    gemm64(pw, rowmajor(B5), rowmajor(B4).tr(), [&](int r, int c, float v) {  // W = Ddot21' - L21 tril(Ddot11)^T
-      sts(el(B0, r, c), lds(el(B0, r, c)) - v);
+    gemm64<true>(pw, rowmajor(B5), rowmajor(B4).tr(), [&](int r, int c, float v) {  // W = Ddot21' - L21 tril(Ddot11)^T
+      sts(el(B0, r, c), rnd(lds(el(B0, r, c)) - v));
     });
+    Tile64 q0, q1;
+    q0.load(Di22, ldi, pt, false);
+    q1.load(D22, ldl, pt, true);
     panel_sync();
     q2.store(B4, pt);  // Ddot22' (tril(Ddot11) consumed)
-    gemm64(pw, rowmajor(B0), rowmajor(B2).tr(), [&](int r, int c, float v) {  // Ddot21 = W D11^{-T}
-      sts(el(B3, r, c), v);
+    gemm64<true>(pw, rowmajor(B0), rowmajor(B2).tr(), [&](int r, int c, float v) {  // Ddot21 = W D11^{-T}
+      sts(el(B3, r, c), rnd(v));
       A21[r + int64_t(c) * lda] = v;
       if (S) S[64 + r + int64_t(c) * lds_] = v;
     });
     panel_sync();
-    q1.store(B1, pt);  // D22
-    q0.store(B2, pt);  // D22^{-1}
+    q1.store(B1, pt, true);  // D22
+    q0.store(B2, pt, true);  // D22^{-1}
     gemm64x2(pw, rowmajor(B3), rowmajor(B5).tr(), rowmajor(B5), rowmajor(B3).tr(),
              [&](int r, int c, float v) {  // Ddot22' -= tril(Ddot21 L21^T + L21 Ddot21^T)
                if (r >= c) sts(el(B4, r, c), lds(el(B4, r, c)) - v);
