@@ -681,6 +681,9 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
 // fp32 batches with 128-wide panels: the diagonal blocks on k_rf_diag128, the 128-wide inverses built
 // from 64-wide ones (CD_NO_DIAG128: the fp64-DMMA sweeps and inverses of width 128 instead)
 static bool g_no_diag128 = getenv("CD_NO_DIAG128") != nullptr;
+// measurement switch: the 128-wide inverses as fp64-DMMA 64-wide ones + a 3xTF32 completion on a side
+// stream (the round-2 route before k_rf_trinv128)
+static bool g_old_inv128 = getenv("CD_OLD_INV128") != nullptr;
 static bool diag128_route(int n, int nb, const Opnd& L) {
   return nb == 128 && n % 128 == 0 && !L.arr && !g_no_diag128 && !g_no_hmma_diag;
 }
@@ -697,9 +700,18 @@ template <typename T>
 static void run_trinv(Ctx& c, int n, int nb, bool reverse, int64_t batch, Opnd L, T* Dinv, bool combine = true) {
   if (c.plan || !c.ok()) return;
   const int nblk = nblocks(n, nb);
+  if (sizeof(T) == 4 && diag128_route(n, nb, L) && !g_old_inv128) {
+    // all 128-wide inverses in one launch (recursive doubling in fp32 / 3xTF32, rf32_fused.cu)
+    c.pre(CD_PROF_TRINV, 0.0);
+    c.err = note_cuda(rf32_trinv128(n, batch, reinterpret_cast<const float*>(static_cast<const T*>(L.base) + L.off),
+                                    L.ld, L.stride, reinterpret_cast<float*>(Dinv), c.st));
+    ++g_launches;
+    if (g_prof.on && !g_prof.recs.empty()) cudaEventRecord(g_prof.recs.back().b, c.st);
+    return;
+  }
   if (sizeof(T) == 4 && diag128_route(n, nb, L)) {
-    // the 64-wide inverses straight onto the diagonals of the 128-wide blocks, then the
-    // lower-left blocks (rf32_inv128)
+    // (CD_OLD_INV128) the 64-wide inverses straight onto the diagonals of the 128-wide blocks, then
+    // the lower-left blocks (rf32_inv128)
     const size_t smem = dmma_cta_smem(8);
     set_smem(k_trinv_dmma<T>, smem);
     c.pre(CD_PROF_TRINV, 0.0);
@@ -2264,7 +2276,7 @@ int cd_chol_rev_fwd_strided_batched(cd_dtype dt, int64_t n, const void* L, int64
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream), side = g_side[dev].s;
   const int snb = shared_dinv_nb(dt, n, batch, o);
   const Opnd Lop{L, nullptr, strideL, ldl, 0};
-  const bool split_inv = snb && dt == CD_F32 && diag128_route(int(n), snb, Lop);
+  const bool split_inv = snb && dt == CD_F32 && diag128_route(int(n), snb, Lop) && g_old_inv128;
   if (split_inv && !g_side[dev].s2 && (r = note_cuda(cudaStreamCreateWithFlags(&g_side[dev].s2, cudaStreamNonBlocking))))
     return r;
   struct ExtReset {  // the shared-inverse hand-over is scoped to this call, error returns included

@@ -62,11 +62,11 @@ constexpr int STAGES = 4;
 constexpr uint32_t A_BYTES = 128 * BK * 4;  // 16 KB
 constexpr uint32_t B_BYTES = BK * NBK * 4;  // 8 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int PLD = 68;                     // pitch (floats) of the 64 x 64 buffers (row-major)
-constexpr int SCR = NBK * PLD;              // floats per 64 x 64 buffer (17 KB)
+constexpr int PLD = 72;                     // pitch (floats) of the 64 x 64 buffers (row-major, swizzled: el())
+constexpr int SCR = NBK * PLD;              // floats per 64 x 64 buffer (18 KB)
 constexpr int NBUF = 7;
 constexpr size_t RING_BYTES = size_t(STAGES) * STAGE_BYTES;  // 96 KB
-constexpr size_t BUF_BYTES = size_t(NBUF) * SCR * 4;         // 119 KB
+constexpr size_t BUF_BYTES = size_t(NBUF) * SCR * 4;         // 126 KB
 constexpr size_t SMEM = 1024 + RING_BYTES + BUF_BYTES + 256;  // + alignment + barriers
 constexpr int THREADS = 320;
 constexpr int W_P0 = 2;                     // first panel warp
@@ -100,16 +100,42 @@ __device__ __forceinline__ float lds(uint32_t a) {
 __device__ __forceinline__ void sts(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(a), "f"(v)); }
 __device__ __forceinline__ float rnd(float x) { return tf32_rna(x); }
 
-// a matrix view in shared memory: element (r, c) at byte address base + 4 (r rs + c cs)
+// 64 x 64 buffers: row-major, pitch 72, the low three column bits XOR-ed with sw(R) = 5 ((R >> 2) & 1):
+// (R, C) at R * 72 + (C & ~7) + ((C & 7) ^ sw(R)).  Bank conflict free for every access the kernels
+// make -- mma.sync fragments of either orientation (8 rows x 4 columns and 4 rows x 8 columns per
+// quarter of the warp), accumulator stores (rows g, g + 4 land on opposite column parities), and 8 x 4
+// element blocks (tile_rc) in either orientation -- and, the swizzle only touching bits below 8,
+// additive: moving by a multiple of 8 rows or columns is a constant byte offset.  (Pitch 68 without
+// a swizzle: 2-way conflicts on MN-major fragments and 4-way on column stores, half of the shared
+// wavefronts of k_rf_diag128.)
+__device__ __forceinline__ int sw64(int R) { return 5 * ((R >> 2) & 1); }
+__device__ __forceinline__ uint32_t el(uint32_t buf, int r, int c) {
+  return buf + 4u * uint32_t(r * PLD + (c & ~7) + ((c & 7) ^ sw64(r)));
+}
+// the element block of panel thread pt in pass q (0..15) of a 64 x 64 sweep: warp w takes rows
+// 8w .. 8w+7, pass q columns 4q .. 4q+3 (a warp: 8 rows x 4 columns, conflict free both ways)
+__device__ __forceinline__ void tile_rc(int pt, int q, int& r, int& c) {
+  r = 8 * (pt >> 5) + (pt & 7);
+  c = 4 * q + ((pt >> 3) & 3);
+}
+// a matrix view of a buffer: logical (r, c) is physical (R0 + r, C0 + c), or (R0 + c, C0 + r)
+// when transposed (t)
 struct SV {
-  uint32_t base;
-  int rs, cs;
-  __device__ __forceinline__ uint32_t at(int r, int c) const { return base + 4u * uint32_t(r * rs + c * cs); }
-  __device__ __forceinline__ SV sub(int r, int c) const { return SV{at(r, c), rs, cs}; }
-  __device__ __forceinline__ SV tr() const { return SV{base, cs, rs}; }  // transpose
+  uint32_t buf;
+  int R0, C0;
+  bool t;
+  __device__ __forceinline__ uint32_t at(int r, int c) const {
+    return t ? el(buf, R0 + c, C0 + r) : el(buf, R0 + r, C0 + c);
+  }
+  __device__ __forceinline__ SV sub(int r, int c) const {
+    return t ? SV{buf, R0 + c, C0 + r, t} : SV{buf, R0 + r, C0 + c, t};
+  }
+  __device__ __forceinline__ SV tr() const { return SV{buf, R0, C0, !t}; }  // transpose
+  // byte offsets of a logical move by 8 rows / 8 columns (additive: multiples of 8)
+  __device__ __forceinline__ uint32_t rstep8() const { return t ? 32u : 32u * PLD; }
+  __device__ __forceinline__ uint32_t cstep8() const { return t ? 32u * PLD : 32u; }
 };
-__device__ __forceinline__ SV rowmajor(uint32_t base) { return SV{base, PLD, 1}; }
-__device__ __forceinline__ uint32_t el(uint32_t buf, int r, int c) { return buf + 4u * uint32_t(r * PLD + c); }
+__device__ __forceinline__ SV rowmajor(uint32_t base) { return SV{base, 0, 0, false}; }
 
 // ---------------------------------------------------------------- mma.sync tf32 helpers
 __device__ __forceinline__ uint32_t rna(float x) {
@@ -130,18 +156,33 @@ struct Frag {
   float a[4];
   float b[NT][2];
 };
-template <int NT>
-__device__ __forceinline__ void frag_load(Frag<NT>& f, const SV& A, const SV& B, int k0) {
+// per-thread fragment base addresses of a view pair (k-step 0, n-tile 0); every other k-step /
+// n-tile is a constant offset from these (the swizzle is additive in steps of 8)
+struct FragBase {
+  uint32_t a0, a2, b0, b1;  // A(g, t), A(g, t + 4), B(t, g), B(t + 4, g)
+  uint32_t ar8, ak8, bk8, bn8;
+};
+__device__ __forceinline__ FragBase frag_base(const SV& A, const SV& B) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  f.a[0] = lds(A.at(g, k0 + t));
-  f.a[1] = lds(A.at(g + 8, k0 + t));
-  f.a[2] = lds(A.at(g, k0 + t + 4));
-  f.a[3] = lds(A.at(g + 8, k0 + t + 4));
+  return FragBase{A.at(g, t), A.at(g, t + 4), B.at(t, g), B.at(t + 4, g), A.rstep8(), A.cstep8(), B.rstep8(),
+                  B.cstep8()};
+}
+template <int NT>
+__device__ __forceinline__ void frag_load(Frag<NT>& f, const FragBase& fb, int k0) {
+  const uint32_t ka = (k0 >> 3) * fb.ak8, kb = (k0 >> 3) * fb.bk8;
+  f.a[0] = lds(fb.a0 + ka);
+  f.a[1] = lds(fb.a0 + fb.ar8 + ka);
+  f.a[2] = lds(fb.a2 + ka);
+  f.a[3] = lds(fb.a2 + fb.ar8 + ka);
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    f.b[nt][0] = lds(B.at(k0 + t, nt * 8 + g));
-    f.b[nt][1] = lds(B.at(k0 + t + 4, nt * 8 + g));
+    f.b[nt][0] = lds(fb.b0 + kb + nt * fb.bn8);
+    f.b[nt][1] = lds(fb.b1 + kb + nt * fb.bn8);
   }
+}
+template <int NT>
+__device__ __forceinline__ void frag_load(Frag<NT>& f, const SV& A, const SV& B, int k0) {
+  frag_load(f, frag_base(A, B), k0);
 }
 // PRE: the operands in shared memory are already tf32-rounded (cvt.rna at store), no conversion here
 template <int NT, bool PRE = false>
@@ -159,11 +200,13 @@ __device__ __forceinline__ void frag_mma(float (&acc)[NT][4], const Frag<NT>& f)
 template <int NT, bool PRE = false>
 __device__ __forceinline__ void warp_mma(float (&acc)[NT][4], int K, const SV& A, const SV& B) {
   Frag<NT> f0, f1;
-  frag_load(f0, A, B, 0);
+  const FragBase fb = frag_base(A, B);
+  frag_load(f0, fb, 0);
+#pragma unroll 1
   for (int k0 = 0; k0 < K; k0 += 16) {
-    frag_load(f1, A, B, k0 + 8);
+    frag_load(f1, fb, k0 + 8);
     frag_mma<NT, PRE>(acc, f0);
-    if (k0 + 16 < K) frag_load(f0, A, B, k0 + 16);
+    if (k0 + 16 < K) frag_load(f0, fb, k0 + 16);
     frag_mma<NT, PRE>(acc, f1);
   }
 }
@@ -205,16 +248,18 @@ __device__ __forceinline__ void gemm64(int pw, const SV& A, const SV& B, FOUT ou
 struct Tile64 {
   float v[16];
   __device__ __forceinline__ void load(const float* src, int64_t ld, int pt, bool tril) {
+    int i, c0;
+    tile_rc(pt, 0, i, c0);
+    const float* p0 = src + i + int64_t(c0) * ld;  // pass q: 4q columns further
+    const int64_t step = 4 * ld;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int e = pt + q * PANEL_THREADS, i = e & 63, c = e >> 6;
-      v[q] = (!tril || i >= c) ? __ldcg(src + i + int64_t(c) * ld) : 0.f;
-    }
+    for (int q = 0; q < 16; ++q) v[q] = (!tril || i >= c0 + 4 * q) ? __ldcg(p0 + q * step) : 0.f;
   }
   __device__ __forceinline__ void store(uint32_t buf, int pt, bool round = false) const {
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      const int e = pt + q * PANEL_THREADS, i = e & 63, c = e >> 6;
+      int i, c;
+      tile_rc(pt, q, i, c);
       sts(el(buf, i, c), round ? rnd(v[q]) : v[q]);
     }
   }
@@ -511,8 +556,9 @@ __device__ void rev_panel(const Params& p, const Step& st, uint32_t tacc, uint32
   gemm64(pw, rowmajor(bC).tr(), rowmajor(bLb), [&](int r, int c, float v) { sts(el(bC2, r, c), v); });
   panel_sync();
   // Psym = Phi(P) + Phi(P)^T: strict lower mirrored, diagonal P_ii -> bL0
-  for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {
-    const int i = e >> 6, j = e & 63;
+  for (int q = 0; q < 16; ++q) {
+    int i, j;
+    tile_rc(pt, q, i, j);
     sts(el(bL0, i, j), i >= j ? lds(el(bC2, i, j)) : lds(el(bC2, j, i)));
   }
   panel_sync();
@@ -568,8 +614,9 @@ __device__ void fwd_panel(const Params& p, const Step& st, uint32_t tacc, uint32
   }
   tmr.lap(PF_LOAD);
   // F3 (Eq. 8): Ddot_sym (mirror of the lower triangle) -> bT
-  for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {
-    const int i = e >> 6, c = e & 63;
+  for (int q = 0; q < 16; ++q) {
+    int i, c;
+    tile_rc(pt, q, i, c);
     sts(el(bT, i, c), i >= c ? lds(el(bIn, i, c)) : lds(el(bIn, c, i)));
   }
   panel_sync();
@@ -737,8 +784,9 @@ __device__ __forceinline__ void eq10_64(int pw, int pt, uint32_t bD, uint32_t bD
                                         uint32_t bU, F out) {
   gemm64<true>(pw, rowmajor(bD).tr(), rowmajor(bIn), [&](int r, int c, float v) { sts(el(bT, r, c), v); });  // P
   panel_sync();
-  for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Psym
-    const int i = e >> 6, j = e & 63;
+  for (int q = 0; q < 16; ++q) {  // Psym
+    int i, j;
+    tile_rc(pt, q, i, j);
     sts(el(bU, i, j), rnd(i >= j ? lds(el(bT, i, j)) : lds(el(bT, j, i))));
   }
   panel_sync();
@@ -752,8 +800,9 @@ __device__ __forceinline__ void eq10_64(int pw, int pt, uint32_t bD, uint32_t bD
 // Ddot = D Phi(D^{-1} Ddot'_sym D^{-T}) (lower triangular: zero above the diagonal)
 template <class F>
 __device__ __forceinline__ void eq8_64(int pw, int pt, uint32_t bD, uint32_t bDi, uint32_t bIn, uint32_t bT, F out) {
-  for (int e = pt; e < NBK * NBK; e += PANEL_THREADS) {  // Ddot'_sym
-    const int i = e >> 6, c = e & 63;
+  for (int q = 0; q < 16; ++q) {  // Ddot'_sym
+    int i, c;
+    tile_rc(pt, q, i, c);
     sts(el(bT, i, c), rnd(i >= c ? lds(el(bIn, i, c)) : lds(el(bIn, c, i))));
   }
   panel_sync();
@@ -827,7 +876,7 @@ __device__ __forceinline__ void gemm64x2(int pw, const SV& A1, const SV& B1, con
 //   fwd:  Ddot11 = Eq8(D11, Ddot11');  Ddot21 = (Ddot21' - L21 tril(Ddot11)^T) D11^{-T};
 //         Ddot22' -= tril(Ddot21 L21^T + L21 Ddot21^T);  Ddot22 = Eq8(D22, Ddot22')
 //         S (128 x 128) = tril(Ddot), zeros above
-// Six 64 x 64 buffers (104 KB): two CTAs per SM.  The next step's operands are prefetched into
+// Six 64 x 64 buffers (108 KB): two CTAs per SM.  The next step's operands are prefetched into
 // registers while the current step's products run.
 __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_diag128(const Diag64 q) {
   extern __shared__ __align__(16) unsigned char smem_d128[];
@@ -975,19 +1024,19 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
 }
 // one warp: acc[16 x 32] += A[16 x 64] B[64 x 32] in 3xTF32
 __device__ __forceinline__ void warp_mma3(float (&acc)[4][4], const SV& A, const SV& B) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const FragBase fb = frag_base(A, B);
 #pragma unroll 2
   for (int k0 = 0; k0 < NBK; k0 += 8) {
+    Frag<4> f;
+    frag_load(f, fb, k0);
     uint32_t ah[4], al[4];
-    split_tf32(lds(A.at(g, k0 + t)), ah[0], al[0]);
-    split_tf32(lds(A.at(g + 8, k0 + t)), ah[1], al[1]);
-    split_tf32(lds(A.at(g, k0 + t + 4)), ah[2], al[2]);
-    split_tf32(lds(A.at(g + 8, k0 + t + 4)), ah[3], al[3]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_tf32(f.a[i], ah[i], al[i]);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       uint32_t bh[2], bl[2];
-      split_tf32(lds(B.at(k0 + t, nt * 8 + g)), bh[0], bl[0]);
-      split_tf32(lds(B.at(k0 + t + 4, nt * 8 + g)), bh[1], bl[1]);
+      split_tf32(f.b[nt][0], bh[0], bl[0]);
+      split_tf32(f.b[nt][1], bh[1], bl[1]);
       mma8(acc[nt], al, bh);
       mma8(acc[nt], ah, bl);
       mma8(acc[nt], ah, bh);
@@ -1037,6 +1086,162 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_rf_inv128(int nblk2, const fl
   zero(acc);
   warp_mma3(acc, rowmajor(b2).sub(r0, 0), rowmajor(b1).sub(0, c0));  // D22^{-1} T
   for_acc(acc, [&](int r, int c, float v) { X[64 + r0 + r + (c0 + c) * 128] = -v; });
+}
+
+// one warp: acc[16 x 8 NT] += A[16 x K] B[K x 8 NT] in 3xTF32 (K a multiple of 8)
+template <int NT>
+__device__ __forceinline__ void warp_mma3k(float (&acc)[NT][4], int K, const SV& A, const SV& B) {
+  const FragBase fb = frag_base(A, B);
+#pragma unroll 1
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    Frag<NT> f;
+    frag_load(f, fb, k0);
+    uint32_t ah[4], al[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_tf32(f.a[i], ah[i], al[i]);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      uint32_t bh[2], bl[2];
+      split_tf32(f.b[nt][0], bh[0], bl[0]);
+      split_tf32(f.b[nt][1], bh[1], bl[1]);
+      mma8(acc[nt], al, bh);
+      mma8(acc[nt], ah, bl);
+      mma8(acc[nt], ah, bh);
+    }
+  }
+}
+
+// The 128-wide diagonal-block inverses of the layered fp32 schedule in one kernel, one CTA of 256
+// threads per 128 x 128 block (the inverses the panel solves C D^{-1} and the Eq. 10 / Eq. 8 block
+// steps use), by recursive doubling on the block:
+//   [D11 0; L21 D22]^{-1} = [X11 0; X21 X22],  X21 = -X22 (L21 X11)
+// applied at widths 16 -> 32 -> 64 -> 128: the sixteen 16 x 16 diagonal inverses by forward
+// substitution in fp32 (one thread per column), every combination on mma.sync in 3xTF32
+// (fp32-faithful products).  Replaces the fp64-DMMA 64-wide inverses + k_rf_inv128 (two launches,
+// ~300 us for configs[3]).  Buffers: D11, L21, D22 and X11, X21, X22 (six swizzled 64 x 64 tiles,
+// 108 KB: two CTAs per SM).  Out: Dinv, 128 x 128 blocks (ld 128), nblk2 per matrix, zero above
+// the diagonal.
+__global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_trinv128(int nblk2, const float* __restrict__ L,
+                                                                   int64_t ldl, int64_t sL, float* __restrict__ Dinv) {
+  extern __shared__ __align__(16) unsigned char smem_t128[];
+  const uint32_t bD1 = smem_u32(smem_t128), bL21 = bD1 + 4 * SCR, bD2 = bL21 + 4 * SCR, bX1 = bD2 + 4 * SCR,
+                 bX21 = bX1 + 4 * SCR, bX2 = bX21 + 4 * SCR;
+  const int pt = threadIdx.x, pw = pt >> 5, lane = pt & 31;
+  const int64_t blk = blockIdx.x;
+  const int64_t b = blk / nblk2;
+  const int Q = int(blk - b * nblk2);
+  const float* D = L + b * sL + 128 * Q + int64_t(128 * Q) * ldl;
+  {
+    Tile64 t0, t1, t2;
+    t0.load(D, ldl, pt, true);                // D11 (zero above the diagonal)
+    t1.load(D + 64, ldl, pt, false);          // L21
+    t2.load(D + 64 + 64 * ldl, ldl, pt, true);  // D22
+    t0.store(bD1, pt);
+    t1.store(bL21, pt);
+    t2.store(bD2, pt);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {  // X buffers start at zero (the upper triangles stay zero)
+      int r, c;
+      tile_rc(pt, q, r, c);
+      sts(el(bX1, r, c), 0.f);
+      sts(el(bX2, r, c), 0.f);
+    }
+  }
+  panel_sync();
+  // width 16: the diagonal 16 x 16 blocks, thread (block, column c): D x = e_c by substitution
+  if (pt < 128) {
+    const int q = pt >> 4, c = pt & 15;
+    const uint32_t bD = q < 4 ? bD1 : bD2, bX = q < 4 ? bX1 : bX2;
+    const int o = 16 * (q & 3);
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float s = (i == c) ? 1.f : 0.f;
+#pragma unroll
+      for (int m = 0; m < i; ++m) s = fmaf(-lds(el(bD, o + i, o + m)), x[m], s);
+      x[i] = (i >= c) ? s / lds(el(bD, o + i, o + i)) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i >= c) sts(el(bX, o + i, o + c), x[i]);
+  }
+  panel_sync();
+  // width 32 (four combinations, warps 0..3) and 64 (two, warps 0..3 as two pairs): T = L21 X11 into
+  // X21's place, then X21 = -X22 T (read fully before the in-place store)
+#pragma unroll 1
+  for (int lev = 0; lev < 2; ++lev) {
+    const int h = lev == 0 ? 16 : 32;  // width of the halves being combined
+    float acc[4][4];
+    zero(acc);
+    bool on = false;
+    uint32_t bD = 0, bX = 0;
+    int o = 0, rr = 0;
+    if (lev == 0 && pw < 4) {  // combination pw: half pw >> 1, 32-block pw & 1; one warp, 16 x 16
+      on = true;
+      bD = pw < 2 ? bD1 : bD2, bX = pw < 2 ? bX1 : bX2, o = 32 * (pw & 1), rr = 0;
+    } else if (lev == 1 && pw < 4) {  // combination pw >> 1, rows 16 (pw & 1); 16 x 32 per warp
+      on = true;
+      bD = pw < 2 ? bD1 : bD2, bX = pw < 2 ? bX1 : bX2, o = 0, rr = 16 * (pw & 1);
+    }
+    const SV L21v = SV{bD, o + h + rr, o, false}, X11v = SV{bX, o, o, false};
+    const SV X22v = SV{bX, o + h + rr, o + h, false}, Tv = SV{bX, o + h, o, false};
+    if (on) {
+      if (lev == 0) {
+        float a2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        warp_mma3k<2>(a2, h, L21v, X11v);
+        for_acc(a2, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), v); });
+      } else {
+        warp_mma3k<4>(acc, h, L21v, X11v);
+        for_acc(acc, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), v); });
+      }
+    }
+    panel_sync();
+    if (on) {
+      if (lev == 0) {
+        float a2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        warp_mma3k<2>(a2, h, X22v, Tv);
+        panel_sync();
+        for_acc(a2, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), -v); });
+      } else {
+        zero(acc);
+        warp_mma3k<4>(acc, h, X22v, Tv);
+        panel_sync();
+        for_acc(acc, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), -v); });
+      }
+    } else {
+      panel_sync();
+    }
+    panel_sync();
+  }
+  // width 128: T = L21 X11 (8 warps, 16 x 32 each) -> bX21, then X21 = -X22 T in place
+  const int r0 = 16 * (pw >> 1), c0 = 32 * (pw & 1);
+  {
+    float acc[4][4];
+    zero(acc);
+    warp_mma3k<4>(acc, NBK, rowmajor(bL21).sub(r0, 0), rowmajor(bX1).sub(0, c0));
+    for_acc(acc, [&](int r, int c, float v) { sts(el(bX21, r0 + r, c0 + c), v); });
+  }
+  panel_sync();
+  {
+    float acc[4][4];
+    zero(acc);
+    warp_mma3k<4>(acc, NBK, rowmajor(bX2).sub(r0, 0), rowmajor(bX21).sub(0, c0));
+    panel_sync();
+    for_acc(acc, [&](int r, int c, float v) { sts(el(bX21, r0 + r, c0 + c), -v); });
+  }
+  panel_sync();
+  // out: [X11 0; X21 X22], coalesced along columns
+  float* X = Dinv + blk * (128 * 128);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    int r, c;
+    tile_rc(pt, q, r, c);
+    X[r + c * 128] = lds(el(bX1, r, c));
+    X[r + (64 + c) * 128] = 0.f;
+    X[64 + r + c * 128] = lds(el(bX21, r, c));
+    X[64 + r + (64 + c) * 128] = lds(el(bX2, r, c));
+  }
+  (void)lane;
 }
 
 // Block inverses D_J^{-1} (fp32 forward substitution, one CTA of 64 threads per 64 x 64 block;
@@ -1226,6 +1431,18 @@ cudaError_t rf32_diag128(bool rev, int64_t batch, const float* L, int64_t ldl, i
     attr = true;
   }
   k_rf_diag128<<<unsigned(batch), PANEL_THREADS, smem, st>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t rf32_trinv128(int n, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* Dinv, cudaStream_t st) {
+  const int nblk2 = n / 128;
+  constexpr size_t smem = 6 * rf::SCR * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rf::k_rf_trinv128, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  rf::k_rf_trinv128<<<unsigned(batch * nblk2), rf::PANEL_THREADS, smem, st>>>(nblk2, L, ldl, sL, Dinv);
   return cudaGetLastError();
 }
 

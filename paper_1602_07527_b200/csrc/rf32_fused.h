@@ -48,5 +48,7 @@ cudaError_t rf32_diag128(bool rev, int64_t batch, const float* L, int64_t ldl, i
 // Complete the 128-wide block inverses (128 x 128 each, ld 128, n / 128 per matrix, consecutive)
 // whose 64-wide diagonal blocks are in place: lower-left block from L, upper-right zero.
 cudaError_t rf32_inv128(int n, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* Dinv, cudaStream_t st);
+// all 128-wide inverses of the layered fp32 route in one launch (recursive doubling, 3xTF32 products)
+cudaError_t rf32_trinv128(int n, int64_t batch, const float* L, int64_t ldl, int64_t sL, float* Dinv, cudaStream_t st);
 
 }  // namespace cd
