@@ -568,6 +568,36 @@ class L2Flush:
         self.buf.fill_(float(self.k))
 
 
+def graph_device_us(call, flush, restore, stream, dist, pairs=20, reps=10):
+    """Device microseconds per call: a CUDA graph of `pairs` (flush, call) pairs against a graph
+    of the flushes alone, both replayed `reps` times between CUDA events (median each)."""
+    import torch
+    restore()
+    torch.cuda.synchronize()
+    g_both, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_both):
+        for _ in range(pairs):
+            flush()
+            call()
+    with torch.cuda.graph(g_flush):
+        for _ in range(pairs):
+            flush()
+
+    def med(g):
+        ts = []
+        for _ in range(reps + 2):
+            restore()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts[2:])
+
+    return dist.max(1e3 * (med(g_both) - med(g_flush)) / pairs)
+
+
 def cpu_oracle_single(kind: str, L, X, reps_seconds=2.0):
     """Oracle (plain C, ONE thread) on one matrix, repeated for about `reps_seconds`:
     kind 'rev' or 'fwd'.  Returns seconds per call."""
@@ -625,10 +655,16 @@ def bench_small_configs(args, dist: Dist):
         cd.chol_rev(Ld, A)
     gms = timed_steps(g.replay, r0, 50, args.warmup, dist, stream)
     tg = dist.max(statistics.median(gms))
+    # device time per call: one CUDA graph holding 20 (L2 flush, call) pairs, minus a graph of the 20
+    # flushes alone (no host submission gap between the events; the calls still start cold)
+    td = graph_device_us(lambda: cd.chol_rev(Ld, A), lambda: flush(), r0, stream, dist)
     out["n64_rev"] = {"workload": "configs[0]: chol_rev fp64 N=64, seed 0", "us_per_call": round(t * 1e3, 2),
                       "gflops": round(rev_flops(64) / (t * 1e-3) / 1e9, 2),
-                      "us_per_call_cuda_graph": round(tg * 1e3, 2), "l2": "flushed before every timed call",
-                      "generator": GEN}
+                      "us_per_call_cuda_graph": round(tg * 1e3, 2),
+                      "us_per_call_device": round(td, 2),
+                      "device_method": "20 (L2 flush, call) pairs captured in one CUDA graph, minus the same "
+                                       "graph of flushes alone, / 20 (median of 10 replays each)",
+                      "l2": "flushed before every timed call", "generator": GEN}
     if cpu:
         sec, reps = cpu_oracle_single("rev", L, Lb)
         out["n64_rev"]["cpu_baseline"] = {"value": round(sec * 1e6, 2), "unit": "us per call", "cores": 1,
@@ -652,7 +688,11 @@ def bench_small_configs(args, dist: Dist):
     tf = dist.max(statistics.median(timed_steps(lambda: cd.chol_fwd(Ld, F), rf, 10, args.warmup, dist, stream)))
     ts = dist.max(statistics.median(timed_steps(lambda: cd.chol_rev(Ld, A, route="symbolic"), ra,
                                                 5, args.warmup, dist, stream)))
+    tdr = graph_device_us(lambda: cd.chol_rev(Ld, A), lambda: flush(), ra, stream, dist, pairs=10) * 1e-3
+    tdf = graph_device_us(lambda: cd.chol_fwd(Ld, F), lambda: flush(), rf, stream, dist, pairs=10) * 1e-3
     out["n1024"] = {"workload": "configs[1]: fp64 N=1024, seed 0", "rev_ms": round(tr, 3), "fwd_ms": round(tf, 3),
+                    "rev_ms_device": round(tdr, 3), "fwd_ms_device": round(tdf, 3),
+                    "device_method": "10 (L2 flush, call) pairs in one CUDA graph minus the flushes alone, / 10",
                     "rev_symbolic_route_ms": round(ts, 3),
                     "rev_gflops": round(rev_flops(1024) / (tr * 1e-3) / 1e9, 1),
                     "fwd_gflops": round(fwd_flops(1024) / (tf * 1e-3) / 1e9, 1),

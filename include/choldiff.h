@@ -245,6 +245,11 @@ int cd_version(void);
 int64_t cd_launch_count(void);
 void cd_reset_launch_count(void);
 
+/* Measurement only: enable (1) / disable (0) clock64 stamps at the phase boundaries of CTA 0 of the
+ * on-chip sweep kernels (one global flag load per boundary) and copy the last stamps (up to `max`,
+ * at most 40) to host memory `out` (may be NULL).  Synchronous (cudaMemcpy*Symbol). */
+int cd_debug_phase_clocks(int enable, long long* out, int max);
+
 /* Kernel-class timing (measurement evidence for bench.py's roofline).  While
  * enabled, the library brackets every launch it enqueues on this thread with a
  * pair of CUDA events on the launch stream and records the launch's ALGORITHMIC

@@ -668,8 +668,13 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
     // 32 < n <= 128: N_b = 8 blocked sweep on DMMA tiles (fp64 arithmetic), one CTA per matrix
     const size_t smem = dmma_cta_smem((n + 7) / 8);
     if (rev) {
-      set_smem(k_rev_dmma_cta<T>, smem);
-      k_rev_dmma_cta<T><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+      if ((n + 7) / 8 == 8) {  // n = 57 .. 64: compile-time block count
+        set_smem(k_rev_dmma_cta<T, 8>, smem);
+        k_rev_dmma_cta<T, 8><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+      } else {
+        set_smem(k_rev_dmma_cta<T>, smem);
+        k_rev_dmma_cta<T><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+      }
     } else {
       set_smem(k_fwd_dmma_cta<T>, smem);
       k_fwd_dmma_cta<T><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, S, info);
@@ -2565,5 +2570,15 @@ int cd_profile_read(int cls, double* ms, double* flops, int64_t* launches) {
   return CD_SUCCESS;
 }
 void cd_reset_launch_count(void) { g_launches = 0; }
+
+int cd_debug_phase_clocks(int enable, long long* out, int max) {
+  if (cudaMemcpyToSymbol(g_dc_clk_on, &enable, sizeof(int)) != cudaSuccess) return CD_ERR_CUDA;
+  if (out && max > 0) {
+    long long tmp[40];
+    if (cudaMemcpyFromSymbol(tmp, g_dc_clk, sizeof(tmp)) != cudaSuccess) return CD_ERR_CUDA;
+    for (int i = 0; i < max && i < 40; ++i) out[i] = tmp[i];
+  }
+  return CD_SUCCESS;
+}
 
 }  // extern "C"

@@ -1089,11 +1089,12 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_rf_inv128(int nblk2, const fl
 }
 
 // one warp: acc[16 x 8 NT] += A[16 x K] B[K x 8 NT] in 3xTF32 (K a multiple of 8)
+// (k-steps [k_lo, k_hi) only: the caller skips the zero blocks of a triangular operand)
 template <int NT>
-__device__ __forceinline__ void warp_mma3k(float (&acc)[NT][4], int K, const SV& A, const SV& B) {
+__device__ __forceinline__ void warp_mma3k(float (&acc)[NT][4], int k_lo, int k_hi, const SV& A, const SV& B) {
   const FragBase fb = frag_base(A, B);
 #pragma unroll 1
-  for (int k0 = 0; k0 < K; k0 += 8) {
+  for (int k0 = k_lo; k0 < k_hi; k0 += 8) {
     Frag<NT> f;
     frag_load(f, fb, k0);
     uint32_t ah[4], al[4];
@@ -1188,10 +1189,10 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_trinv128(int nblk2, con
     if (on) {
       if (lev == 0) {
         float a2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        warp_mma3k<2>(a2, h, L21v, X11v);
+        warp_mma3k<2>(a2, 0, h, L21v, X11v);
         for_acc(a2, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), v); });
       } else {
-        warp_mma3k<4>(acc, h, L21v, X11v);
+        warp_mma3k<4>(acc, 0, h, L21v, X11v);
         for_acc(acc, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), v); });
       }
     }
@@ -1199,12 +1200,12 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_trinv128(int nblk2, con
     if (on) {
       if (lev == 0) {
         float a2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        warp_mma3k<2>(a2, h, X22v, Tv);
+        warp_mma3k<2>(a2, 0, h, X22v, Tv);
         panel_sync();
         for_acc(a2, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), -v); });
       } else {
         zero(acc);
-        warp_mma3k<4>(acc, h, X22v, Tv);
+        warp_mma3k<4>(acc, 0, rr + 16, X22v, Tv);  // X22 rows rr..rr+15: zero beyond column rr+15
         panel_sync();
         for_acc(acc, [&](int r, int c, float v) { sts(Tv.sub(rr, 0).at(r, c), -v); });
       }
@@ -1218,14 +1219,14 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_rf_trinv128(int nblk2, con
   {
     float acc[4][4];
     zero(acc);
-    warp_mma3k<4>(acc, NBK, rowmajor(bL21).sub(r0, 0), rowmajor(bX1).sub(0, c0));
+    warp_mma3k<4>(acc, c0, NBK, rowmajor(bL21).sub(r0, 0), rowmajor(bX1).sub(0, c0));  // X11(k, c) = 0 for k < c
     for_acc(acc, [&](int r, int c, float v) { sts(el(bX21, r0 + r, c0 + c), v); });
   }
   panel_sync();
   {
     float acc[4][4];
     zero(acc);
-    warp_mma3k<4>(acc, NBK, rowmajor(bX2).sub(r0, 0), rowmajor(bX21).sub(0, c0));
+    warp_mma3k<4>(acc, 0, r0 + 16, rowmajor(bX2).sub(r0, 0), rowmajor(bX21).sub(0, c0));  // X22(r, k) = 0 for k > r
     panel_sync();
     for_acc(acc, [&](int r, int c, float v) { sts(el(bX21, r0 + r, c0 + c), -v); });
   }

@@ -43,6 +43,15 @@ __device__ __forceinline__ int tat(int NBLK, int i, int m) {
 #ifndef CD_DC_MINB
 #define CD_DC_MINB 4  // 64 registers: 4 CTAs per SM at n <= 64 (batched fp32 diagonal blocks: -5 %)
 #endif
+// phase clocks of CTA 0 of the on-chip sweeps (measurement only: cd_debug_phase_clocks; off unless
+// CD_DEBUG_CLK is set, then one global load per phase boundary)
+__device__ int g_dc_clk_on = 0;
+__device__ long long g_dc_clk[40];
+// (the flag is read once per CTA into dc_clk_on; stamps are taken by thread 0 of CTA 0 only)
+#define dc_clk(i)                                                      \
+  do {                                                                 \
+    if (dc_clk_on) g_dc_clk[i] = clock64();                            \
+  } while (0)
 constexpr int DC_NMAX = 128;  // largest n (and diagonal block) handled on chip
 constexpr int DC_WARPS = 8;
 constexpr int DC_THREADS = DC_WARPS * 32;
@@ -60,8 +69,27 @@ __device__ __forceinline__ void dc_stage(int NBLK, const TIO* __restrict__ g, in
   const int NP = 8 * NBLK, NTILE = NBLK * (NBLK + 1) / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if constexpr (sizeof(TIO) == 8) {
-    for (int m = warp; m < n; m += DC_WARPS)
-      for (int i = m + lane; i < n; i += 32) cp_async_zfill<8>(s + tat(NBLK, i, m), g + i + int64_t(m) * ld, true);
+    if ((ld & 1) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+      // 16-byte copies of row pairs (i, i + 1), i even: a pair lands on two consecutive swizzled
+      // slots of one tile (t8 only flips bit 2 of the row).  Odd columns start with their diagonal
+      // element alone, so nothing above the diagonal is fetched.
+      for (int m = warp; m < n; m += DC_WARPS) {
+        const double* gc = g + int64_t(m) * ld;
+        if ((m & 1) && lane == 0) cp_async_zfill<8>(s + tat(NBLK, m, m), gc + m, true);
+        for (int i = ((m + 1) & ~1) + 2 * lane; i < n; i += 64) {
+          if (i + 1 < n) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s + tat(NBLK, i, m)));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gc + i) : "memory");
+          } else {
+            cp_async_zfill<8>(s + tat(NBLK, i, m), gc + i, true);
+          }
+        }
+      }
+
+    } else {
+      for (int m = warp; m < n; m += DC_WARPS)
+        for (int i = m + lane; i < n; i += 32) cp_async_zfill<8>(s + tat(NBLK, i, m), g + i + int64_t(m) * ld, true);
+    }
   } else {
     // fp32: all loads of a group of 4 columns are issued before the first convert / store
     // (one-by-one, every column cost a full memory latency: 30-40 % of the stall samples)
@@ -145,6 +173,19 @@ template <typename TIO>
 __device__ __forceinline__ void dc_store(int NBLK, TIO* __restrict__ g, int64_t ld, int n, const double* s,
                                          int out_mode) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (sizeof(TIO) == 8 && out_mode == 0 && (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+    // tril only, row pairs as 16-byte stores (odd columns: the diagonal element alone)
+    for (int m = warp; m < n; m += DC_WARPS) {
+      TIO* gc = g + int64_t(m) * ld;
+      if ((m & 1) && lane == 0) gc[m] = TIO(s[tat(NBLK, m, m)]);
+      for (int i = ((m + 1) & ~1) + 2 * lane; i < n; i += 64) {
+        const double* sp = s + tat(NBLK, i, m);
+        if (i + 1 < n) *reinterpret_cast<double2*>(gc + i) = *reinterpret_cast<const double2*>(sp);
+        else gc[i] = TIO(sp[0]);
+      }
+    }
+    return;
+  }
   for (int m = warp; m < n; m += DC_WARPS)
     for (int i = m + lane; i < n; i += 32) {
       double v = s[tat(NBLK, i, m)];
@@ -162,10 +203,13 @@ __device__ __forceinline__ void dc_store(int NBLK, TIO* __restrict__ g, int64_t 
 }
 
 // ============================================================================ reverse
-template <typename TIO>
+// NB_ > 0: the block count is a compile-time constant (n = 8 NB_ - 7 .. 8 NB_), so the tile
+// indexing and the per-step work lists fold away (single small matrices: the launch latency is
+// the whole cost)
+template <typename TIO, int NB_ = 0>
 __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
     k_rev_dmma_cta(int n, Opnd Ld, Opnd Ad, int out_mode, Opnd Sd, int* __restrict__ info) {
-  const int NBLK = (n + 7) >> 3;
+  const int NBLK = NB_ ? NB_ : (n + 7) >> 3;
   const int NP = 8 * NBLK;
   const int NTILE = NBLK * (NBLK + 1) / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -182,19 +226,27 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
   const TIO* L = optr<TIO>(Ld, b);
   TIO* A = optr_w<TIO>(Ad, b);
 
+  const bool dc_clk_on = blockIdx.x == 0 && tid == 0 && *const_cast<volatile int*>(&g_dc_clk_on);
+  dc_clk(0);
   if (tid == 0) *sbad = 0x7fffffff;
   dc_stage<TIO>(NBLK, L, Ld.ld, n, sL, true);
+  dc_clk(37);
   dc_stage<TIO>(NBLK, A, Ad.ld, n, sA, false);
+  dc_clk(38);
   cp_async_wait_all();
+  dc_clk(39);
   __syncthreads();
+  dc_clk(1);
   dc_diag_inverses(NBLK, sL, sDi, sRd, n, sbad);
   if (tid == 0 && info) info[b] = (*sbad == 0x7fffffff) ? 0 : *sbad;
+  dc_clk(2);
 
   for (int J = NBLK - 1; J >= 0; --J) {
     const int PT = NBLK - 1 - J, QT = J;
     const double* Di = sDi + J * 64;
     double* Dt = sA + tile_base(NBLK, J, J);
     const double* Lt = sL + tile_base(NBLK, J, J);
+    dc_clk(3 + 4 * (NBLK - 1 - J));
 
     // s1: Cbar <- Cbar D^{-1}
     for (int rt = warp; rt < PT; rt += DC_WARPS) {
@@ -207,6 +259,7 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
       Ct[t8(g, 2 * t + 1)] = c1;
     }
     __syncthreads();
+    dc_clk(4 + 4 * (NBLK - 1 - J));
 
     // s3 (last warp): Dbar <- Dbar - tril(Cbar^T C);   s2 (all warps): Bbar <- Bbar - Cbar R
     if (warp == DC_WARPS - 1 && PT > 0) {
@@ -222,6 +275,22 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
       if (g >= 2 * t) Dt[t8(g, 2 * t)] -= a0;
       if (g >= 2 * t + 1) Dt[t8(g, 2 * t + 1)] -= a1;
     }
+    // s5a (warps from the top, one per column tile): Rbar <- Rbar - Cbar^T B -- independent of the
+    // diagonal block, so only S R is left after s4 (the R column tile J-1 is the next step's
+    // critical path).  Warps below take the s2 tiles.
+    for (int ct = DC_WARPS - 2 - warp; warp < DC_WARPS - 1 && PT > 0 && ct < QT; ct += DC_WARPS - 1) {
+      double* Rb = sA + tile_base(NBLK, J, ct);
+      double c0 = Rb[t8(g, 2 * t)], c1 = Rb[t8(g, 2 * t + 1)];
+      double d0 = 0.0, d1 = 0.0;
+      for (int rt = 0; rt < PT; ++rt) {
+        const double* Ct = sA + tile_base(NBLK, J + 1 + rt, J);
+        const double* Bt = sL + tile_base(NBLK, J + 1 + rt, ct);
+        dmma884(c0, c1, Ct[t8(t, g)], -Bt[t8(t, g)]);
+        dmma884(d0, d1, Ct[t8(4 + t, g)], -Bt[t8(4 + t, g)]);
+      }
+      Rb[t8(g, 2 * t)] = c0 + d0;
+      Rb[t8(g, 2 * t + 1)] = c1 + d1;
+    }
     for (int idx = warp; idx < PT * QT; idx += DC_WARPS) {
       const int rt = idx / QT, ct = idx - rt * QT;
       const double* Ct = sA + tile_base(NBLK, J + 1 + rt, J);
@@ -234,6 +303,7 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
       Bt[t8(g, 2 * t + 1)] = c1;
     }
     __syncthreads();
+    dc_clk(5 + 4 * (NBLK - 1 - J));
 
     // s4 (warp 0): Y = D^{-T}(P + P^T)D^{-1}, P = Phi(D^T Dbar); S = Y; tril(Dbar) = Phi(Y)
     if (warp == 0) {
@@ -268,28 +338,24 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
       if (g >= c1i) Dt[t8(g, c1i)] = (g == c1i) ? 0.5 * y1 : y1;
     }
     __syncthreads();
+    dc_clk(6 + 4 * (NBLK - 1 - J));
 
-    // s5: Rbar <- Rbar - Cbar^T B - S R
+    // s5b: Rbar <- Rbar - S R   (the Cbar^T B part ran in s5a)
     for (int ct = warp; ct < QT; ct += DC_WARPS) {
       double* Rb = sA + tile_base(NBLK, J, ct);
       const double* Rt = sL + tile_base(NBLK, J, ct);
       double c0 = Rb[t8(g, 2 * t)], c1 = Rb[t8(g, 2 * t + 1)];
-      double d0 = 0.0, d1 = 0.0;
-      for (int rt = 0; rt < PT; ++rt) {
-        const double* Ct = sA + tile_base(NBLK, J + 1 + rt, J);
-        const double* Bt = sL + tile_base(NBLK, J + 1 + rt, ct);
-        dmma884(c0, c1, Ct[t8(t, g)], -Bt[t8(t, g)]);
-        dmma884(d0, d1, Ct[t8(4 + t, g)], -Bt[t8(4 + t, g)]);
-      }
 #pragma unroll
-      for (int kk = 0; kk < 2; ++kk) dmma884(d0, d1, sS[t8(g, 4 * kk + t)], -Rt[t8(4 * kk + t, g)]);
-      Rb[t8(g, 2 * t)] = c0 + d0;
-      Rb[t8(g, 2 * t + 1)] = c1 + d1;
+      for (int kk = 0; kk < 2; ++kk) dmma884(c0, c1, sS[t8(g, 4 * kk + t)], -Rt[t8(4 * kk + t, g)]);
+      Rb[t8(g, 2 * t)] = c0;
+      Rb[t8(g, 2 * t + 1)] = c1;
     }
     __syncthreads();
   }
 
+  dc_clk(35);
   dc_store<TIO>(NBLK, A, Ad.ld, n, sA, out_mode);
+  dc_clk(36);
   if (Sd.base || Sd.arr) {  // S = Dbar + Dbar^T (diagonal doubled), dense
     TIO* S = optr_w<TIO>(Sd, b);
     for (int c = warp; c < n; c += DC_WARPS)
