@@ -354,6 +354,9 @@ static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
 static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
 static int g_tc_bn64 = getenv("CD_TC_BN64") ? atoi(getenv("CD_TC_BN64")) : 1;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
+// measurement switch: k_rev_bulk32<4>'s register budget as minimum CTAs per SM (default 3: 166
+// registers, three CTAs per SM; 4 = 128 registers and four CTAs, measured 12 % slower)
+static int g_b32_minb = getenv("CD_B32_MINB") ? atoi(getenv("CD_B32_MINB")) : 3;
 // fp32 64-wide diagonal blocks of the layered schedule on the mma.sync Eq. 10 / Eq. 8 kernel of
 // rf32_fused.cu (default; configs[3] launch list: 41.6 vs 51.5 us per launch of 1024 blocks) or on
 // the fp64-DMMA on-chip sweeps (CD_NO_HMMA_DIAG=1).  The block inverses stay on k_trinv_dmma
@@ -635,7 +638,8 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
       if (nblk == 1) launch(k_rev_bulk32<1>, b32_smem<1>());
       else if (nblk == 2) launch(k_rev_bulk32<2>, b32_smem<2>());
       else if (nblk == 3) launch(k_rev_bulk32<3>, b32_smem<3>());
-      else launch(k_rev_bulk32<4>, b32_smem<4>());
+      else if (g_b32_minb == 4) launch(k_rev_bulk32<4, 4>, b32_smem<4>());
+      else launch(k_rev_bulk32<4, 3>, b32_smem<4>());
     } else if (rev && sizeof(T) == 8) {
       // fp64 reverse: register-resident N_b = 8 blocked sweep on DMMA tiles (sweep_reg32.cuh)
       const int nblk = (n + 7) / 8;
