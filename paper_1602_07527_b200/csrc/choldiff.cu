@@ -999,6 +999,10 @@ static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DE
 // (N = 4096: 5.53 -> 5.24 ms with 16; N = 1024 and 16384 unchanged; 4 and 8 were slower)
 static int64_t g_fs_pieces = getenv("CD_FS_PIECES") ? atoi(getenv("CD_FS_PIECES")) : 16;
 static bool g_no_bal1 = getenv("CD_NO_BAL1") != nullptr;  // forward panel: one CTA per 128-wide K chunk
+// reverse panel phase 1: 128-row tiles cut into up to this many sub-tiles when the panel has few
+// tiles (1 = whole tiles, and the 32 x 32-tile path for the fewest).  Measured with 4 against 1:
+// N = 16384 93.24 -> 92.36 ms, 8192 16.27 -> 15.43 ms, 4096 4.08 -> 3.73 ms, 1024 487 -> 466 us
+static int g_pr_split = getenv("CD_PR_SPLIT") ? atoi(getenv("CD_PR_SPLIT")) : 4;
 
 static std::atomic<int> g_panel_occ[kMaxDev];
 static int panel_occupancy() {
@@ -1018,7 +1022,9 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
   double* Sall = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * s_stride));
   double* llpart = static_cast<double*>(c.take(sizeof(double) * size_t(c.sms) * 2 * LL_TILE));
   int* cnt = static_cast<int*>(c.take(sizeof(int) * size_t(batch) * nblk));
-  double* prpart = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
+  // P partial slots: one per 128-row tile, or per sub-tile when phase 1 splits (then all fit one grid)
+  const size_t nslots = std::max<size_t>(size_t(batch) * nblk, size_t(c.sms) * panel_occupancy());
+  double* prpart = static_cast<double*>(c.take(sizeof(double) * nslots * 128 * 128));
   double* Pws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   double* Zws = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * 128 * 128));
   double* Wst = static_cast<double*>(c.take(sizeof(double) * size_t(batch) * nblk * 128 * 128));
@@ -1115,6 +1121,7 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pp.Sall = Sall;
     pp.s_blk = int64_t(LL_BM + 4) * LL_BM;
     pp.nblk = nblk;
+    pp.split_max = g_pr_split;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs
     void* args[] = {&pp};
     const double wf = w;

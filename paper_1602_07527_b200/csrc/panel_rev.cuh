@@ -61,6 +61,7 @@ struct PanelParams {
   const double* Sall;    // S blocks (ld s_ld, block stride s_blk, batch stride s_stride) = diagonal tiles of M
   int64_t s_blk;
   int nblk;              // S slot of the block at row r0: nblk - (n - r0) / 128
+  int split_max;         // phase 1: 128-row tiles split into up to this many sub-tiles (1, 2, 4)
 };
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
@@ -169,13 +170,161 @@ __device__ __forceinline__ void pr_tile32(double* sm, FA fa, FB fb, EP ep) {
   pr_tile32k(sm, 128, fa, fb, ep);
 }
 
-__global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p) {
-  extern __shared__ __align__(16) unsigned char smem_pr[];
-  double* sm = reinterpret_cast<double*>(smem_pr);
+// Phase 1 of k_panel_rev on sub-tiles of ROWS = 16 RT rows (RT = 8: whole 128-row tiles; 4 / 2:
+// halves / quarters, s = 128 / ROWS of them per tile, when the panel has few tiles):
+//   step A  W = Cbar_sub D^{-1}  (stored in place and kept in shared memory)
+//   step C  P_sub = tril(W^T C_sub)  (K = ROWS), stored to its own partial slot (s per tile)
+template <int RT>
+__device__ __forceinline__ void pr_phase1_units(const PanelParams& p, double* sm, int64_t nunits, int s) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // warp -> (wm, wn): the SM sub-partition (warp & 3) gets one column group from each
   // end, so the triangular work of step A is balanced across sub-partitions
   const int wm = warp >> 2, wn = wm == 0 ? (warp & 3) : 3 - (warp & 3), g = lane >> 2, t = lane & 3;
+  const int w = p.w;
+  constexpr int ROWS = 16 * RT;  // rows of a sub-tile; each warp owns ROWS / 2 of them in step A
+  const int64_t nsl = int64_t(p.tiles) * s;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t b = u / nsl;
+    const int st_ = int(u - b * nsl), tl = st_ / s, h = st_ - tl * s;
+    const int r0 = p.k + 128 * tl + ROWS * h;
+    double* Cb = optr_w<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;     // Cbar sub-tile (ROWS x w)
+    const double* Ct = optr<double>(p.L, b) + r0 + int64_t(p.j) * p.L.ld;  // C tile
+    const double* Di = p.Dinv + b * p.dstride;
+
+    // ---------------- step A: W = Cbar_t D^{-1} ----------------
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    const int nkc = (w + PR_BK - 1) / PR_BK;
+    auto load_a = [&](int st, int kc) {
+      double* as = sm + st * (PR_A_SIZE + PR_B_SIZE);
+      double* bs = as + PR_A_SIZE;
+      for (int e = tid; e < PR_BK * ROWS; e += PR_THREADS) {
+        const int m = e % ROWS, kx = e / ROWS;  // A: Cbar[m, kc + kx]
+        const int kk = kc * PR_BK + kx;
+        cp_async8(as + kx * PR_KM_PITCH + m, Cb + m + int64_t(min(kk, w - 1)) * p.A.ld, kk < w);
+      }
+      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
+        const int kx = e % PR_BK, nn = e / PR_BK;  // B: Dinv[kc + kx, nn]
+        const int kk = kc * PR_BK + kx;
+        const bool ok = kk < w && nn < w;
+        cp_async8(bs + nn * PR_NK_PITCH + kx, Di + (ok ? kk + int64_t(nn) * p.dld : 0), ok);
+      }
+    };
+#pragma unroll 1
+    for (int q = 0; q < PR_STAGES - 1; ++q) {
+      if (q < nkc) load_a(q, q);
+      cp_async_commit();
+    }
+#pragma unroll 1
+    for (int kc = 0; kc < nkc; ++kc) {
+      cp_async_wait<PR_STAGES - 2>();
+      __syncthreads();
+      if (kc + PR_STAGES - 1 < nkc) load_a((kc + PR_STAGES - 1) % PR_STAGES, kc + PR_STAGES - 1);
+      cp_async_commit();
+      // D^{-1}[kk, c] = 0 for kk < c: this chunk reaches columns c <= kc*16 + 15 only
+      if (kc * PR_BK + PR_BK - 1 >= wn * 32) {
+        const double* as = sm + (kc % PR_STAGES) * (PR_A_SIZE + PR_B_SIZE);
+        const double* bs = as + PR_A_SIZE;
+#pragma unroll
+        for (int kq = 0; kq < PR_BK / 4; ++kq) {
+          const int kx = kq * 4 + t;
+          double a[RT], bb[4];
+#pragma unroll
+          for (int i = 0; i < RT; ++i) a[i] = as[kx * PR_KM_PITCH + wm * (ROWS / 2) + i * 8 + g];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[(wn * 32 + jj * 8 + g) * PR_NK_PITCH + kx];
+#pragma unroll
+          for (int i = 0; i < RT; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
+        }
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();  // stage buffers dead: W and the step C stages alias them
+    double* Ws = sm;
+    double* Cs = sm + 128 * PR_W_PITCH;
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wm * (ROWS / 2) + i * 8 + g;
+          const int c = wn * 32 + jj * 8 + 2 * t + e;
+          Ws[r + c * PR_W_PITCH] = acc[i][jj][e];  // columns >= w are exactly 0
+          if (c < w) Cb[r + int64_t(c) * p.A.ld] = acc[i][jj][e];
+        }
+
+    // ---------------- step C: P_t = tril(W^T C_t) ----------------
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    auto load_c = [&](int st, int rc) {
+      double* bs = Cs + st * PR_B_SIZE;
+      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
+        const int kx = e % PR_BK, nn = e / PR_BK;  // B: C[rc*16 + kx, nn]
+        const bool ok = nn < w;
+        cp_async8(bs + nn * PR_NK_PITCH + kx, Ct + (rc * PR_BK + kx) + int64_t(ok ? nn : 0) * p.L.ld, ok);
+      }
+    };
+    constexpr int NRC = ROWS / PR_BK;  // K of step C = the sub-tile's rows
+#pragma unroll 1
+    for (int q = 0; q < PR_STAGES - 1; ++q) {
+      if (q < NRC) load_c(q, q);
+      cp_async_commit();
+    }
+    const bool active = wm * 64 + 63 >= wn * 32;  // some a >= b in this warp's tile
+#pragma unroll 1
+    for (int rc = 0; rc < NRC; ++rc) {
+      cp_async_wait<PR_STAGES - 2>();
+      __syncthreads();
+      if (rc + PR_STAGES - 1 < NRC) load_c((rc + PR_STAGES - 1) % PR_STAGES, rc + PR_STAGES - 1);
+      cp_async_commit();
+      if (active) {
+        const double* bs = Cs + (rc % PR_STAGES) * PR_B_SIZE;
+#pragma unroll
+        for (int kq = 0; kq < PR_BK / 4; ++kq) {
+          const int kx = kq * 4 + t;
+          double a[8], bb[4];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = Ws[(wm * 64 + i * 8 + g) * PR_W_PITCH + rc * PR_BK + kx];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[(wn * 32 + jj * 8 + g) * PR_NK_PITCH + kx];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
+        }
+      }
+    }
+    cp_async_wait_all();
+    double* slot = p.part + u * int64_t(128 * 128);
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = wm * 64 + i * 8 + g;
+            const int c = wn * 32 + jj * 8 + 2 * t + e;
+            if (r >= c) __stcg(slot + r + c * 128, acc[i][jj][e]);
+          }
+    }
+    __syncthreads();  // before the next tile reuses the shared memory
+  }
+
+}
+
+__global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_pr[];
+  double* sm = reinterpret_cast<double*>(smem_pr);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int w = p.w;
   const int64_t units = p.batch * p.tiles;
 
@@ -219,7 +368,14 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   // few tiles (early steps): split every tile's work into 32 x 32 tiles over the grid --
   // 1a: W = Cbar D^{-1} (16 tiles per 128-row tile, staged), grid sync, 1b: the lower
   // 32 x 32 tiles of P_t = W^T C (K = the tile's 128 rows) and W copied back in place
-  const bool small = units * 4 <= int64_t(gridDim.x);
+  // phase 1 split: with few tiles the 128-row tiles are cut into 64- or 32-row sub-tiles so that
+  // more SMs share the work (p.split_max); the 32 x 32-tile path below is the alternative for the
+  // fewest tiles (p.split_max < 4)
+  const bool small = p.split_max < 4 && units * 4 <= int64_t(gridDim.x);
+  const int split = small                                                 ? 1
+                    : p.split_max >= 4 && units * 4 <= int64_t(gridDim.x) ? 4
+                    : p.split_max >= 2 && units * 2 <= int64_t(gridDim.x) ? 2
+                                                                          : 1;
   if (small && !(p.dbg_skip & 1)) {
     const int64_t ua = units * 16;
     for (int64_t u = blockIdx.x; u < ua; u += gridDim.x) {
@@ -277,140 +433,10 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
     }
   }
 
-  for (int64_t u = blockIdx.x; u < units && !small && !(p.dbg_skip & 1); u += gridDim.x) {
-    const int64_t b = u / p.tiles;
-    const int tl = int(u - b * p.tiles);
-    const int r0 = p.k + 128 * tl;
-    double* Cb = optr_w<double>(p.A, b) + r0 + int64_t(p.j) * p.A.ld;     // Cbar tile (128 x w)
-    const double* Ct = optr<double>(p.L, b) + r0 + int64_t(p.j) * p.L.ld;  // C tile
-    const double* Di = p.Dinv + b * p.dstride;
-
-    // ---------------- step A: W = Cbar_t D^{-1} ----------------
-    double acc[8][4][2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
-    const int nkc = (w + PR_BK - 1) / PR_BK;
-    auto load_a = [&](int st, int kc) {
-      double* as = sm + st * (PR_A_SIZE + PR_B_SIZE);
-      double* bs = as + PR_A_SIZE;
-      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
-        const int m = e & 127, kx = e >> 7;  // A: Cbar[m, kc + kx]
-        const int kk = kc * PR_BK + kx;
-        cp_async8(as + kx * PR_KM_PITCH + m, Cb + m + int64_t(min(kk, w - 1)) * p.A.ld, kk < w);
-      }
-      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
-        const int kx = e % PR_BK, nn = e / PR_BK;  // B: Dinv[kc + kx, nn]
-        const int kk = kc * PR_BK + kx;
-        const bool ok = kk < w && nn < w;
-        cp_async8(bs + nn * PR_NK_PITCH + kx, Di + (ok ? kk + int64_t(nn) * p.dld : 0), ok);
-      }
-    };
-#pragma unroll 1
-    for (int s = 0; s < PR_STAGES - 1; ++s) {
-      if (s < nkc) load_a(s, s);
-      cp_async_commit();
-    }
-#pragma unroll 1
-    for (int kc = 0; kc < nkc; ++kc) {
-      cp_async_wait<PR_STAGES - 2>();
-      __syncthreads();
-      if (kc + PR_STAGES - 1 < nkc) load_a((kc + PR_STAGES - 1) % PR_STAGES, kc + PR_STAGES - 1);
-      cp_async_commit();
-      // D^{-1}[kk, c] = 0 for kk < c: this chunk reaches columns c <= kc*16 + 15 only
-      if (kc * PR_BK + PR_BK - 1 >= wn * 32) {
-        const double* as = sm + (kc % PR_STAGES) * (PR_A_SIZE + PR_B_SIZE);
-        const double* bs = as + PR_A_SIZE;
-#pragma unroll
-        for (int kq = 0; kq < PR_BK / 4; ++kq) {
-          const int kx = kq * 4 + t;
-          double a[8], bb[4];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = as[kx * PR_KM_PITCH + wm * 64 + i * 8 + g];
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[(wn * 32 + jj * 8 + g) * PR_NK_PITCH + kx];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
-        }
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();  // stage buffers dead: W and the step C stages alias them
-    double* Ws = sm;
-    double* Cs = sm + 128 * PR_W_PITCH;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = wm * 64 + i * 8 + g;
-          const int c = wn * 32 + jj * 8 + 2 * t + e;
-          Ws[r + c * PR_W_PITCH] = acc[i][jj][e];  // columns >= w are exactly 0
-          if (c < w) Cb[r + int64_t(c) * p.A.ld] = acc[i][jj][e];
-        }
-
-    // ---------------- step C: P_t = tril(W^T C_t) ----------------
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
-    auto load_c = [&](int st, int rc) {
-      double* bs = Cs + st * PR_B_SIZE;
-      for (int e = tid; e < PR_BK * 128; e += PR_THREADS) {
-        const int kx = e % PR_BK, nn = e / PR_BK;  // B: C[rc*16 + kx, nn]
-        const bool ok = nn < w;
-        cp_async8(bs + nn * PR_NK_PITCH + kx, Ct + (rc * PR_BK + kx) + int64_t(ok ? nn : 0) * p.L.ld, ok);
-      }
-    };
-    constexpr int NRC = 128 / PR_BK;
-#pragma unroll 1
-    for (int s = 0; s < PR_STAGES - 1; ++s) {
-      load_c(s, s);
-      cp_async_commit();
-    }
-    const bool active = wm * 64 + 63 >= wn * 32;  // some a >= b in this warp's tile
-#pragma unroll 1
-    for (int rc = 0; rc < NRC; ++rc) {
-      cp_async_wait<PR_STAGES - 2>();
-      __syncthreads();
-      if (rc + PR_STAGES - 1 < NRC) load_c((rc + PR_STAGES - 1) % PR_STAGES, rc + PR_STAGES - 1);
-      cp_async_commit();
-      if (active) {
-        const double* bs = Cs + (rc % PR_STAGES) * PR_B_SIZE;
-#pragma unroll
-        for (int kq = 0; kq < PR_BK / 4; ++kq) {
-          const int kx = kq * 4 + t;
-          double a[8], bb[4];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = Ws[(wm * 64 + i * 8 + g) * PR_W_PITCH + rc * PR_BK + kx];
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[(wn * 32 + jj * 8 + g) * PR_NK_PITCH + kx];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
-        }
-      }
-    }
-    cp_async_wait_all();
-    double* slot = p.part + u * int64_t(128 * 128);
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = wm * 64 + i * 8 + g;
-            const int c = wn * 32 + jj * 8 + 2 * t + e;
-            if (r >= c) __stcg(slot + r + c * 128, acc[i][jj][e]);
-          }
-    }
-    __syncthreads();  // before the next tile reuses the shared memory
+  if (!small && !(p.dbg_skip & 1)) {
+    if (split == 4) pr_phase1_units<2>(p, sm, units * 4, 4);
+    else if (split == 2) pr_phase1_units<4>(p, sm, units * 2, 2);
+    else pr_phase1_units<8>(p, sm, units, 1);
   }
 
   // ---------------- phase 2: Dbar -= sum_t P_t (lower triangle) ----------------
@@ -424,6 +450,7 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
   const int64_t gw = int64_t(blockIdx.x) * (PR_THREADS / 32) + warp;
   const int64_t ntri = int64_t(w) * (w + 1) / 2;
   const int64_t nel = ntri * p.batch;  // lower-triangle entries (a >= c), column-packed
+  const int nsl = p.tiles * split;     // P partial slots per matrix
   const int q = lane & 7;
   for (int64_t wb = gw * 4; wb < nel && !(p.dbg_skip & 2); wb += nwarps * 4) {
     const int64_t el = wb + (lane >> 3);
@@ -443,17 +470,17 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_rev(const PanelParams p
     }
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (on) {
-      const double* pb = p.part + b * p.tiles * int64_t(128 * 128) + a + c * 128;
+      const double* pb = p.part + b * nsl * int64_t(128 * 128) + a + c * 128;
       constexpr int64_t TS = 128 * 128;
       int tl = q;
-      for (; tl + 24 < p.tiles; tl += 32) {  // four independent loads in flight per lane
+      for (; tl + 24 < nsl; tl += 32) {  // four independent loads in flight per lane
         const double x0 = __ldcg(pb + tl * TS), x1 = __ldcg(pb + (tl + 8) * TS);
         const double x2 = __ldcg(pb + (tl + 16) * TS), x3 = __ldcg(pb + (tl + 24) * TS);
         s0 += x0, s1 += x1, s2 += x2, s3 += x3;
       }
-      if (tl < p.tiles) s0 += __ldcg(pb + tl * TS);
-      if (tl + 8 < p.tiles) s1 += __ldcg(pb + (tl + 8) * TS);
-      if (tl + 16 < p.tiles) s2 += __ldcg(pb + (tl + 16) * TS);
+      if (tl < nsl) s0 += __ldcg(pb + tl * TS);
+      if (tl + 8 < nsl) s1 += __ldcg(pb + (tl + 8) * TS);
+      if (tl + 16 < nsl) s2 += __ldcg(pb + (tl + 16) * TS);
     }
     double s = (s0 + s1) + (s2 + s3);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
