@@ -28,6 +28,11 @@ def main():
             cd.chol_rev(dev(L), dev(Lb), route="symbolic")
         S = np.einsum("...ij,...kj->...ik", L, L)
         cd.chol_fwd_fused(dev(S), dev(np.tril(Sd)))
+    # panel phase 1 on 64-row sub-tiles (7 tiles per panel at most) and the batched N = 32 kernel
+    L, Lb, _ = synthetic.draw(1024, 1)
+    cd.chol_rev(dev(L), dev(Lb))
+    L, Lb, _ = synthetic.draw_batch(32, 1000, seed=1)
+    cd.chol_rev(dev(L), dev(Lb))
     torch.cuda.synchronize()
     print("ok")
 
