@@ -246,8 +246,9 @@ int64_t cd_launch_count(void);
 void cd_reset_launch_count(void);
 
 /* Measurement only: enable (1) / disable (0) clock64 stamps at the phase boundaries of CTA 0 of the
- * on-chip sweep kernels (one global flag load per boundary) and copy the last stamps (up to `max`,
- * at most 40) to host memory `out` (may be NULL).  Synchronous (cudaMemcpy*Symbol). */
+ * on-chip reverse sweep for n = 57..64 (while enabled the library launches a separately compiled
+ * instance with the stamps; production launches carry none) and copy the last stamps (up to `max`,
+ * at most 40) to host memory `out` (may be NULL).  Synchronous (cudaMemcpyFromSymbol). */
 int cd_debug_phase_clocks(int enable, long long* out, int max);
 
 /* Kernel-class timing (measurement evidence for bench.py's roofline).  While

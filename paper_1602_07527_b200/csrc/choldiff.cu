@@ -354,6 +354,7 @@ static bool g_tc32_disabled = getenv("CD_DISABLE_TC32") != nullptr;
 static int g_tc_epi = getenv("CD_TC_EPI") ? atoi(getenv("CD_TC_EPI")) : 1;
 static int g_tc_bn64 = getenv("CD_TC_BN64") ? atoi(getenv("CD_TC_BN64")) : 1;
 static bool g_no_bulk32 = getenv("CD_NO_BULK32") != nullptr;
+static std::atomic<bool> g_dc_clk_host{false};  // cd_debug_phase_clocks: the CLK instantiation of k_rev_dmma_cta
 // measurement switch: k_rev_bulk32<4>'s register budget as minimum CTAs per SM (default 3: 166
 // registers, three CTAs per SM; 4 = 128 registers and four CTAs, measured 12 % slower)
 static int g_b32_minb = getenv("CD_B32_MINB") ? atoi(getenv("CD_B32_MINB")) : 3;
@@ -673,8 +674,13 @@ static void run_sweep_small(Ctx& c, bool rev, int n, int64_t batch, Opnd L, Opnd
     const size_t smem = dmma_cta_smem((n + 7) / 8);
     if (rev) {
       if ((n + 7) / 8 == 8) {  // n = 57 .. 64: compile-time block count
-        set_smem(k_rev_dmma_cta<T, 8>, smem);
-        k_rev_dmma_cta<T, 8><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+        if (g_dc_clk_host) {  // phase clocks (cd_debug_phase_clocks)
+          set_smem(k_rev_dmma_cta<T, 8, true>, smem);
+          k_rev_dmma_cta<T, 8, true><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+        } else {
+          set_smem(k_rev_dmma_cta<T, 8>, smem);
+          k_rev_dmma_cta<T, 8><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
+        }
       } else {
         set_smem(k_rev_dmma_cta<T>, smem);
         k_rev_dmma_cta<T><<<unsigned(batch), DC_THREADS, smem, c.st>>>(n, L, A, out_mode, S, info);
@@ -2583,7 +2589,7 @@ int cd_profile_read(int cls, double* ms, double* flops, int64_t* launches) {
 void cd_reset_launch_count(void) { g_launches = 0; }
 
 int cd_debug_phase_clocks(int enable, long long* out, int max) {
-  if (cudaMemcpyToSymbol(g_dc_clk_on, &enable, sizeof(int)) != cudaSuccess) return CD_ERR_CUDA;
+  g_dc_clk_host = enable != 0;
   if (out && max > 0) {
     long long tmp[40];
     if (cudaMemcpyFromSymbol(tmp, g_dc_clk, sizeof(tmp)) != cudaSuccess) return CD_ERR_CUDA;

@@ -43,11 +43,11 @@ __device__ __forceinline__ int tat(int NBLK, int i, int m) {
 #ifndef CD_DC_MINB
 #define CD_DC_MINB 4  // 64 registers: 4 CTAs per SM at n <= 64 (batched fp32 diagonal blocks: -5 %)
 #endif
-// phase clocks of CTA 0 of the on-chip sweeps (measurement only: cd_debug_phase_clocks; off unless
-// CD_DEBUG_CLK is set, then one global load per phase boundary)
-__device__ int g_dc_clk_on = 0;
+// phase clocks of CTA 0 of the on-chip sweeps (measurement only: cd_debug_phase_clocks selects the
+// CLK = true instantiation; stamps are taken by thread 0 of CTA 0 only).  A compile-time switch:
+// a runtime flag read from global memory at kernel start held warp 0 -- and through it the whole
+// staging -- for one memory latency (~1 us with a cold L2) in every production launch.
 __device__ long long g_dc_clk[40];
-// (the flag is read once per CTA into dc_clk_on; stamps are taken by thread 0 of CTA 0 only)
 #define dc_clk(i)                                                      \
   do {                                                                 \
     if (dc_clk_on) g_dc_clk[i] = clock64();                            \
@@ -206,7 +206,7 @@ __device__ __forceinline__ void dc_store(int NBLK, TIO* __restrict__ g, int64_t 
 // NB_ > 0: the block count is a compile-time constant (n = 8 NB_ - 7 .. 8 NB_), so the tile
 // indexing and the per-step work lists fold away (single small matrices: the launch latency is
 // the whole cost)
-template <typename TIO, int NB_ = 0>
+template <typename TIO, int NB_ = 0, bool CLK = false>
 __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
     k_rev_dmma_cta(int n, Opnd Ld, Opnd Ad, int out_mode, Opnd Sd, int* __restrict__ info) {
   const int NBLK = NB_ ? NB_ : (n + 7) >> 3;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(DC_THREADS, CD_DC_MINB)
   const TIO* L = optr<TIO>(Ld, b);
   TIO* A = optr_w<TIO>(Ad, b);
 
-  const bool dc_clk_on = blockIdx.x == 0 && tid == 0 && *const_cast<volatile int*>(&g_dc_clk_on);
+  const bool dc_clk_on = CLK && blockIdx.x == 0 && tid == 0;
   dc_clk(0);
   if (tid == 0) *sbad = 0x7fffffff;
   dc_stage<TIO>(NBLK, L, Ld.ld, n, sL, true);
