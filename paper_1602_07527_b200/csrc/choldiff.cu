@@ -1009,6 +1009,8 @@ static bool g_no_bal1 = getenv("CD_NO_BAL1") != nullptr;  // forward panel: one 
 // tiles (1 = whole tiles, and the 32 x 32-tile path for the fewest).  Measured with 4 against 1:
 // N = 16384 93.24 -> 92.36 ms, 8192 16.27 -> 15.43 ms, 4096 4.08 -> 3.73 ms, 1024 487 -> 466 us
 static int g_pr_split = getenv("CD_PR_SPLIT") ? atoi(getenv("CD_PR_SPLIT")) : 4;
+// forward panel phase 0 (the previous panel's W D^{-T}): the same sub-tile split (1 = 32 x 32 staged tiles)
+static int g_pf_split = getenv("CD_PF_SPLIT") ? atoi(getenv("CD_PF_SPLIT")) : 4;
 
 static std::atomic<int> g_panel_occ[kMaxDev];
 static int panel_occupancy() {
@@ -1364,6 +1366,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pf.skip3 = 0;
     pf.dbg_skip = g_dbg_panel_skip;
     pf.kslot_cap = g_no_bal1 ? 0 : kslots;
+    pf.split_max = g_pf_split;
     const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
     void* args[] = {&pf};
     const double wf = w;
@@ -1491,6 +1494,7 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
     pf.Fws = Fws;
     pf.Dc = Dc;
     pf.kslot_cap = g_no_bal1 ? 0 : kslots;
+    pf.split_max = g_pf_split;
   };
   int j_prev = 0, k_prev = 0, p_prev = 0;
   for (int qb = 0; qb < nblk && c.ok(); ++qb) {

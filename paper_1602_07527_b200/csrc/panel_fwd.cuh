@@ -42,6 +42,7 @@ struct PanelFwdParams {
   int skip3;             // skip phase 3 (Eq. 8)
   int dbg_skip;          // measurement only (CD_DEBUG_PANEL_SKIP): bit i skips phase i; results wrong
   int kslot_cap;         // phase 1 partial slots available per batch entry (balanced K split, batch 1)
+  int split_max;         // phase 0: 128-row tiles cut into up to this many sub-tiles (1, 2, 4)
 };
 
 // acc (64 x 32 warp tiles of a 128 x 128 tile) += sum over K of A(m, kk) B(kk, c), K in
@@ -49,9 +50,11 @@ struct PanelFwdParams {
 // (zero).  skip(kc) (warp-uniform) drops a chunk for this warp.  Stage layout As[k][m],
 // Bs[k][c], pitch 132 (conflict-free fragments).  Used when a phase has enough 128-wide
 // units to fill the GPU (fewer operand re-reads than 32 x 32 tiles).
-template <class FA, class FB, class SK>
+// RT < 8: only the first ROWS = 16 RT rows of A (the warp tiles shrink to ROWS / 2 x 32; acc rows
+// i < RT are used)
+template <int RT = 8, class FA, class FB, class SK>
 __device__ __forceinline__ void pf_prod128(double* sm, int K, FA fa, FB fb, SK skip, double (&acc)[8][4][2]) {
-  constexpr int P = 132, STG = 2 * 16 * P;
+  constexpr int P = 132, STG = 2 * 16 * P, ROWS = 16 * RT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3, g = lane >> 2, t = lane & 3;
   const int nkc = (K + 15) / 16;
@@ -61,11 +64,11 @@ __device__ __forceinline__ void pf_prod128(double* sm, int K, FA fa, FB fb, SK s
     for (int e = tid; e < 16 * 128; e += PR_THREADS) {
       const int m = e & 127, kx = e >> 7;
       const int kk = kc * 16 + kx;
-      const double* pa = kk < K ? fa(m, kk) : nullptr;
+      const double* pa = (kk < K && m < ROWS) ? fa(m, kk) : nullptr;
       const double* pb = kk < K ? fb(kk, m) : nullptr;
       // no source -> a zero by a plain shared store (never a zero-size copy from a dummy address)
       if (pa) cp_async8(as + kx * P + m, pa, true);
-      else as[kx * P + m] = 0.0;
+      else if (m < ROWS) as[kx * P + m] = 0.0;
       if (pb) cp_async8(bs + kx * P + m, pb, true);
       else bs[kx * P + m] = 0.0;
     }
@@ -88,19 +91,57 @@ __device__ __forceinline__ void pf_prod128(double* sm, int K, FA fa, FB fb, SK s
 #pragma unroll
       for (int kq = 0; kq < 4; ++kq) {
         const int kx = kq * 4 + t;
-        double a[8], bb[4];
+        double a[RT], bb[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = as[kx * P + wm * 64 + i * 8 + g];
+        for (int i = 0; i < RT; ++i) a[i] = as[kx * P + wm * (ROWS / 2) + i * 8 + g];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) bb[jj] = bs[kx * P + wn * 32 + jj * 8 + g];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < RT; ++i)
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
       }
     }
   }
   cp_async_wait_all();
+}
+
+// Phase 0 on sub-tiles of ROWS = 16 RT rows (RT = 8: whole 128-row tiles), s = 128 / ROWS per tile:
+// Cdot_rows <- W_rows D_prev^{-T} in place (a CTA reads all 128 columns of its rows before writing)
+template <int RT>
+__device__ __forceinline__ void pf_phase0_units(const PanelFwdParams& p, double* sm, int64_t nunits, int s) {
+  constexpr int ROWS = 16 * RT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3, g = lane >> 2, t = lane & 3;
+  const int64_t nsub = int64_t(p.tiles_prev) * s;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t b = u / nsub;
+    const int st_ = int(u - b * nsub), tl = st_ / s, h = st_ - tl * s;
+    const int r0 = p.k_prev + 128 * tl + ROWS * h;
+    double* Wt = optr_w<double>(p.T0, b) + r0 + int64_t(p.j_prev) * p.T0.ld;
+    const double* Di = p.Dinv_prev + b * p.dstride;
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    pf_prod128<RT>(
+        sm, 128,
+        [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.T0.ld : nullptr; },
+        [&](int kk, int c) -> const double* { return c >= kk ? Di + c + int64_t(kk) * p.dld : nullptr; },
+        [&](int kc) { return kc * 16 > wn * 32 + 31; },  // D^{-T}(kk, c) = 0 for kk > c
+        acc);
+    __syncthreads();  // every warp has read its W rows before any is overwritten
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wm * (ROWS / 2) + i * 8 + g, c = wn * 32 + jj * 8 + 2 * t + e;
+          if (r0 + r < p.n) Wt[r + int64_t(c) * p.T0.ld] = acc[i][jj][e];
+        }
+  }
 }
 
 __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParams p) {
@@ -111,40 +152,21 @@ __global__ void __launch_bounds__(PR_THREADS, 1) k_panel_fwd(const PanelFwdParam
   namespace cg = cooperative_groups;
 
   // ---------------- phase 0: previous panel  Cdot <- W D_prev^{-T} ----------------
-  // 32 x 32 output tiles (16 per 128-row tile), so small panels still spread over the GPU
-  const bool big0 = p.batch * p.tiles_prev >= int64_t(gridDim.x) / 2;
+  // whole 128-row tiles when there are enough of them; otherwise 64- / 32-row sub-tiles
+  // (p.split_max), or 32 x 32 output tiles staged through global memory (p.split_max < 2 or
+  // fewer than 16 tiles)
+  const int64_t units0 = p.batch * p.tiles_prev;
+  const int s0 = p.split_max >= 4 && units0 * 4 <= int64_t(gridDim.x)   ? 4
+                 : p.split_max >= 2 && units0 * 2 <= int64_t(gridDim.x) ? 2
+                                                                        : 1;
+  // (below 16 tiles the 32 x 32 staged tiles win: a sub-tile loads all of D^{-T} for few rows --
+  // N = 1024 forward 680 vs 722 us)
+  const bool big0 = (s0 > 1 && units0 >= 16) || units0 >= int64_t(gridDim.x) / 2;
   const bool ph0 = p.Dinv_prev && !(p.dbg_skip & 1);
-  if (ph0 && big0) {  // one CTA per 128-row tile
-    const int lane_ = threadIdx.x & 31, wm = warp >> 2, wn = warp & 3, g = lane_ >> 2, t = lane_ & 3;
-    const int64_t units = p.batch * p.tiles_prev;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const int64_t b = u / p.tiles_prev;
-      const int tl = int(u - b * p.tiles_prev);
-      const int r0 = p.k_prev + 128 * tl;
-      double* Wt = optr_w<double>(p.T0, b) + r0 + int64_t(p.j_prev) * p.T0.ld;
-      const double* Di = p.Dinv_prev + b * p.dstride;
-      double acc[8][4][2];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
-      pf_prod128(
-          sm, 128,
-          [&](int m, int kk) -> const double* { return r0 + m < p.n ? Wt + m + int64_t(kk) * p.T0.ld : nullptr; },
-          [&](int kk, int c) -> const double* { return c >= kk ? Di + c + int64_t(kk) * p.dld : nullptr; },
-          [&](int kc) { return kc * 16 > wn * 32 + 31; },  // D^{-T}(kk, c) = 0 for kk > c
-          acc);
-      __syncthreads();  // every warp has read its W rows before any is overwritten
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = wm * 64 + i * 8 + g, c = wn * 32 + jj * 8 + 2 * t + e;
-            if (r0 + r < p.n) Wt[r + int64_t(c) * p.T0.ld] = acc[i][jj][e];
-          }
-    }
+  if (ph0 && big0) {
+    if (s0 == 4) pf_phase0_units<2>(p, sm, units0 * 4, 4);
+    else if (s0 == 2) pf_phase0_units<4>(p, sm, units0 * 2, 2);
+    else pf_phase0_units<8>(p, sm, units0, 1);
     __threadfence();
     cg::this_grid().sync();
   } else if (ph0) {

@@ -19,7 +19,7 @@ to = lambda m: torch.from_numpy(synthetic.to_colmajor(m)).cuda().transpose(0, 1)
 Ld, A0, F0 = to(L), to(Lb), to(np.tril(Sd))
 A = A0.clone()
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-for name, fn, src in (("rev", cd.chol_rev, A0), ("fwd", cd.chol_fwd, F0)):
+for name, fn, src in ((("rev", cd.chol_rev, A0), ("fwd", cd.chol_fwd, F0)) if os.environ.get("ONLY") is None else [x for x in (("rev", cd.chol_rev, A0), ("fwd", cd.chol_fwd, F0)) if x[0] == os.environ["ONLY"]]):
     ts = []
     for i in range(25):
         A.copy_(src)
