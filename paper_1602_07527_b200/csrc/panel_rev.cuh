@@ -36,7 +36,7 @@ constexpr int PR_B_SIZE = 128 * PR_NK_PITCH;    // 2560
 constexpr int PR_W_PITCH = 132;
 constexpr size_t PR_SMEM_A = size_t(PR_STAGES) * (PR_A_SIZE + PR_B_SIZE) * 8;              // step A stages
 constexpr size_t PR_SMEM_C = size_t(128) * PR_W_PITCH * 8 + size_t(PR_STAGES) * PR_B_SIZE * 8;  // W + step C stages
-constexpr size_t PR_SMEM = PR_SMEM_A > PR_SMEM_C ? PR_SMEM_A : PR_SMEM_C;
+constexpr size_t PR_SMEM_AC = PR_SMEM_A > PR_SMEM_C ? PR_SMEM_A : PR_SMEM_C;
 
 struct PanelParams {
   Opnd A, L;         // Abar and L (whole matrices)
@@ -78,7 +78,11 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {  // all but the n most 
     case 4: cp_async_wait<4>(); break;
     case 5: cp_async_wait<5>(); break;
     case 6: cp_async_wait<6>(); break;
-    default: cp_async_wait<7>(); break;
+    case 7: cp_async_wait<7>(); break;
+    case 8: cp_async_wait<8>(); break;
+    case 9: cp_async_wait<9>(); break;
+    case 10: cp_async_wait<10>(); break;
+    default: cp_async_wait<11>(); break;
   }
 }
 
@@ -94,7 +98,14 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {  // all but the n most 
 constexpr int PT_P = 132, PT_PKM = 36;
 constexpr int PT_A = 128 * PT_PKM > 32 * PT_P ? 128 * PT_PKM : 32 * PT_P;  // 4608 doubles
 constexpr int PT_SLOT = 2 * PT_A;                                          // A and B, 9216 doubles
-static_assert(2 * PT_SLOT * 8 <= PR_SMEM, "pr_tile32k buffers exceed the panel kernels' shared memory");
+// K chunks in flight: PT_NSLOT buffers (a third one, 221 KB of shared memory, measured no faster:
+// N = 1024 reverse 468.6 vs 466 us, N = 16384 92.44 vs 92.36 ms -- the tiles are not waiting on L2)
+#ifndef CD_PT_NSLOT
+#define CD_PT_NSLOT 2
+#endif
+constexpr int PT_NSLOT = CD_PT_NSLOT;
+constexpr size_t PR_SMEM = size_t(PT_NSLOT) * PT_SLOT * 8 > PR_SMEM_AC ? size_t(PT_NSLOT) * PT_SLOT * 8 : PR_SMEM_AC;
+static_assert(PR_SMEM <= 232448, "panel kernels' shared memory exceeds the per-CTA limit");
 
 template <class FA, class FB, class EP, class AM, class BN>
 __device__ __forceinline__ void pr_tile32kx(double* sm, int K, FA fa, FB fb, EP ep, AM am, BN bn) {
@@ -103,7 +114,7 @@ __device__ __forceinline__ void pr_tile32kx(double* sm, int K, FA fa, FB fb, EP 
   double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   const int nch = (K + 127) / 128;
   auto load = [&](int ch) {
-    double* As = sm + (ch & 1) * PT_SLOT;
+    double* As = sm + (ch % PT_NSLOT) * PT_SLOT;
     double* Bs = As + PT_A;
     const int kb = 128 * ch;
     const bool mf = am(kb), nf = bn(kb);
@@ -131,17 +142,19 @@ __device__ __forceinline__ void pr_tile32kx(double* sm, int K, FA fa, FB fb, EP 
     }
   };
   __syncthreads();  // shared memory reuse
-  load(0);
+#pragma unroll 1
+  for (int c = 0; c < PT_NSLOT - 1 && c < nch; ++c) load(c);
 #pragma unroll 1
   for (int ch = 0; ch < nch; ++ch) {
-    const bool next = ch + 1 < nch;
-    if (next) load(ch + 1);
-    const double* As = sm + (ch & 1) * PT_SLOT;
+    // chunk ch + NSLOT - 1 goes into the buffer chunk ch - 1 used (freed by the barrier after it)
+    if (ch + PT_NSLOT - 1 < nch) load(ch + PT_NSLOT - 1);
+    const int ahead = min(PT_NSLOT - 1, nch - 1 - ch);  // chunks issued after this one
+    const double* As = sm + (ch % PT_NSLOT) * PT_SLOT;
     const double* Bs = As + PT_A;
     const bool mf = am(128 * ch), nf = bn(128 * ch);
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
-      cp_async_wait_n(3 - q + (next ? 4 : 0));
+      cp_async_wait_n(3 - q + 4 * ahead);
       __syncthreads();
 #pragma unroll
       for (int kq = 8 * q; kq < 8 * q + 8; ++kq) {
@@ -152,7 +165,7 @@ __device__ __forceinline__ void pr_tile32kx(double* sm, int K, FA fa, FB fb, EP 
                   nf ? Bs[(4 * kq + t) * PT_PKM + 8 * (nt0 + u) + g] : Bs[(8 * (nt0 + u) + g) * PT_P + 4 * kq + t]);
       }
     }
-    __syncthreads();  // this buffer is refilled by chunk ch + 2
+    __syncthreads();  // this buffer is refilled by chunk ch + NSLOT
   }
 #pragma unroll
   for (int u = 0; u < 2; ++u)
