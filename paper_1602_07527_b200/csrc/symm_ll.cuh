@@ -110,6 +110,9 @@ __global__ void __launch_bounds__(LL_THREADS, 1) k_symm_ll(const LLParams p, con
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  // launched with programmatic stream serialization (PDL) after the previous panel kernel: the
+  // prologue above overlaps its tail; every global access below waits for it to complete
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   __syncthreads();
 
   if (warp >= LL_CONSUMERS) {
