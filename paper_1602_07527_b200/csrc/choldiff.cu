@@ -258,6 +258,28 @@ static int grid_1d(int64_t total, int threads, int sms) {
 }
 
 // ------------------------------------------------------------------ kernel attribute setup
+static bool g_no_pdl = getenv("CD_NO_PDL") != nullptr;  // measurement: plain launches of the persistent kernels
+// a persistent stream-K kernel launched with programmatic stream serialization (PDL): its CTAs may
+// start (prologue only, then griddepcontrol.wait) as the previous kernel's CTAs exit
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kernel, int grid, int threads, size_t smem, cudaStream_t st, Args... args) {
+  if (g_no_pdl) {
+    kernel<<<grid, threads, smem, st>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <typename K>
 static void set_smem(K kernel, size_t bytes) {
   // opt in well below 48 KB: the 48 KB default limit counts static shared memory too
@@ -565,7 +587,7 @@ struct Gemm {
     static const int tc_sms = getenv("CD_TC_SMS") ? atoi(getenv("CD_TC_SMS")) : 0;
     const int sms = tc_sms > 0 ? std::min(tc_sms, c.sms) : c.sms;
     const unsigned g = unsigned(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(sms) * occ)));
-    kern<<<g, tcp_threads(EPI), smem, c.st>>>(p, tm, em);
+    c.err = note_cuda(launch_pdl(kern, int(g), tcp_threads(EPI), smem, c.st, p, tm, em));
     c.launched();
     return true;
   }
@@ -999,27 +1021,7 @@ static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
 static int64_t g_ll_pieces = getenv("CD_LL_PIECES") ? atoi(getenv("CD_LL_PIECES")) : 8;
 // the SYMM moves into the panel kernel while its 32 x 32 output tiles number <= this x #SMs
 static int64_t g_symm_in_panel = getenv("CD_SYMM_IN_PANEL") ? atoi(getenv("CD_SYMM_IN_PANEL")) : 1;
-static bool g_no_pdl = getenv("CD_NO_PDL") != nullptr;  // measurement: plain launches of k_symm_ll / k_fwd_sk
-// a persistent stream-K kernel launched with programmatic stream serialization (PDL): its CTAs may
-// start (prologue only, then griddepcontrol.wait) as the previous kernel's CTAs exit
-template <typename K, typename... Args>
-static cudaError_t launch_pdl(K kernel, int grid, int threads, size_t smem, cudaStream_t st, Args... args) {
-  if (g_no_pdl) {
-    kernel<<<grid, threads, smem, st>>>(args...);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, args...);
-}
+
 // (the cooperative panel kernels launched with PDL as well measured no faster: N = 16384 reverse
 // 91.95 vs 91.94 ms, forward 95.46 vs 95.45 ms)
 static cudaError_t launch_coop(const void* kernel, unsigned grid, size_t smem, cudaStream_t st, void** args) {

@@ -230,6 +230,9 @@ __global__ void __launch_bounds__(tcp_threads(EPI), EPI ? CD_TC_EPI_MINB : CD_TC
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // launched with programmatic stream serialization (PDL): the prologue above overlaps the previous
+  // kernel's tail; every global access below waits for it to complete
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
