@@ -51,8 +51,14 @@
  *     outputs of that matrix are then unspecified.  Other non-finite inputs are
  *     not checked (finiteness is a precondition).
  *   - n = 0 or batch = 0 is a no-op returning CD_SUCCESS.
- *   - Reentrant; no global mutable state except a per-process cache of kernel
- *     attributes.  L may be shared read-only by concurrent calls.
+ *   - Reentrant from any number of host threads.  Library state: per-device caches
+ *     (kernel attributes, occupancies, SM counts; initialised once, thread-safe);
+ *     per-host-thread, per-device CUDA streams and events that some calls create on
+ *     first use (the lookahead and host-copy streams, chol_rev_fwd's side stream),
+ *     released when the thread exits; per-thread measurement state (launch counter,
+ *     profiling records, last CUDA error text).  Measurement switches are read from
+ *     the environment once per process.  L may be shared read-only by concurrent
+ *     calls; calls that share an output or a workspace must be ordered by the caller.
  */
 #ifndef CHOLDIFF_H
 #define CHOLDIFF_H
