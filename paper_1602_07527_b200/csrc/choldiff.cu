@@ -1031,7 +1031,10 @@ static int g_dbg_panel_skip = getenv("CD_DEBUG_PANEL_SKIP") ? atoi(getenv("CD_DE
 // k_fwd_sk CTAs: at most ~PIECES pieces per output tile (0 = no cap); the cap only binds on the last
 // ~10 panels of a sweep (m < 10 tiles), where the last arriver otherwise sums up to ~30 partial tiles
 // (N = 4096: 5.53 -> 5.24 ms with 16; N = 1024 and 16384 unchanged; 4 and 8 were slower)
-static int64_t g_fs_pieces = getenv("CD_FS_PIECES") ? atoi(getenv("CD_FS_PIECES")) : 16;
+static int64_t g_fs_pieces = getenv("CD_FS_PIECES") ? atoi(getenv("CD_FS_PIECES")) : -1;  // -1: by size
+// (forward N = 16384: 16 -> 32 pieces 95.56 -> 95.05 ms; N = 8192 17.20 -> 17.10 ms; N = 4096 keeps 16:
+// 4.56 vs 4.66 ms with 32)
+static int64_t fs_pieces(int n) { return g_fs_pieces >= 0 ? g_fs_pieces : (n > 4096 ? 32 : 16); }
 static bool g_no_bal1 = getenv("CD_NO_BAL1") != nullptr;  // forward panel: one CTA per 128-wide K chunk
 // reverse panel phase 1: 128-row tiles cut into up to this many sub-tiles when the panel has few
 // tiles (1 = whole tiles, and the 32 x 32-tile path for the fewest).  Measured with 4 against 1:
@@ -1414,7 +1417,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
         return;
       }
       fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
-      if (g_fs_pieces > 0) fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, g_fs_pieces * batch * fp.m)));
+      if (fs_pieces(n) > 0) fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, fs_pieces(n) * batch * fp.m)));
       fp.part = skpart;
       fp.cnt = cnt;
       fp.chol = 0;
@@ -1499,8 +1502,8 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
       return;
     }
     fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
-    if (g_fs_pieces > 0)  // (fused sweep N = 4096: 12.54 -> 12.12 ms)
-      fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, g_fs_pieces * batch * fp.m)));
+    if (fs_pieces(n) > 0)  // (fused sweep N = 4096: 12.54 -> 12.12 ms)
+      fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, fs_pieces(n) * batch * fp.m)));
     fp.part = skpart;
     fp.cnt = cnt;
     fp.chol = chol;
