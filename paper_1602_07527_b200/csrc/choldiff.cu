@@ -1043,6 +1043,11 @@ static int g_pr_split = getenv("CD_PR_SPLIT") ? atoi(getenv("CD_PR_SPLIT")) : 4;
 // forward panel phase 0 (the previous panel's W D^{-T}): the same sub-tile split (1 = 32 x 32 staged tiles)
 static int g_pf_split = getenv("CD_PF_SPLIT") ? atoi(getenv("CD_PF_SPLIT")) : 4;
 
+// measurement: cap on the cooperative panel grid (0 = every co-resident CTA)
+static int64_t g_panel_grid = getenv("CD_PANEL_GRID") ? atoi(getenv("CD_PANEL_GRID")) : 0;
+static unsigned panel_grid(int64_t resident) {
+  return unsigned(g_panel_grid > 0 ? std::min<int64_t>(resident, g_panel_grid) : resident);
+}
 static std::atomic<int> g_panel_occ[kMaxDev];
 static int panel_occupancy() {
   return per_device(g_panel_occ, [] {
@@ -1161,7 +1166,7 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pp.s_blk = int64_t(LL_BM + 4) * LL_BM;
     pp.nblk = nblk;
     pp.split_max = g_pr_split;
-    const unsigned grid = unsigned(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs
+    const unsigned grid = panel_grid(int64_t(c.sms) * panel_occupancy());  // all co-resident CTAs
     void* args[] = {&pp};
     const double wf = w;
     c.pre(CD_PROF_PANEL, (double(p) * w * (w + 1) * 2.0 + (4 * wf * wf * wf + 3 * wf * wf + 11 * wf) / 6) * double(batch));
@@ -1397,7 +1402,7 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
     pf.dbg_skip = g_dbg_panel_skip;
     pf.kslot_cap = g_no_bal1 ? 0 : kslots;
     pf.split_max = g_pf_split;
-    const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
+    const unsigned grid = panel_grid(int64_t(c.sms) * panel_fwd_occupancy());
     void* args[] = {&pf};
     const double wf = w;
     c.pre(CD_PROF_PANEL, (double(p_prev) * 128 * 129 + 2.0 * wf * (wf + 1) * q +
@@ -1483,7 +1488,7 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
   set_smem(k_panel_fwd, PR_SMEM);
   const size_t dsm = dmma_cta_smem((nb + 7) / 8);
   set_smem(k_chol_diag<double>, dsm);
-  const unsigned grid = unsigned(int64_t(c.sms) * panel_fwd_occupancy());
+  const unsigned grid = panel_grid(int64_t(c.sms) * panel_fwd_occupancy());
   auto panel = [&](PanelFwdParams& pf, double flops) {
     void* args[] = {&pf};
     c.pre(CD_PROF_PANEL, flops * double(batch));
