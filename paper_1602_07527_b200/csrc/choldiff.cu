@@ -1019,8 +1019,11 @@ static void blocked_rev_la(Ctx& c, LaStreams* ls, int n, int nb, int64_t batch, 
 // Requires fp64, nb = 128 and TMA-describable Abar / L (16-byte aligned, even ld).
 static bool g_no_ll = getenv("CD_REV_RIGHT_LOOKING") != nullptr;
 static int64_t g_ll_pieces = getenv("CD_LL_PIECES") ? atoi(getenv("CD_LL_PIECES")) : 8;
-// the SYMM moves into the panel kernel while its 32 x 32 output tiles number <= this x #SMs
-static int64_t g_symm_in_panel = getenv("CD_SYMM_IN_PANEL") ? atoi(getenv("CD_SYMM_IN_PANEL")) : 1;
+// the SYMM moves into the panel kernel while its 32 x 32 output tiles number <= this x #SMs.  Default
+// 0 (never) since k_symm_ll's deferred fixup: N = 1024 reverse 465 -> 453 us, 2048 1180 -> 1136 us,
+// 4096 3592 -> 3550 us, 8192 15.26 -> 15.21 ms against 1 (before the deferred fixup, 1 won: 466 vs 602 us)
+static int64_t g_symm_in_panel = getenv("CD_SYMM_IN_PANEL") ? atoi(getenv("CD_SYMM_IN_PANEL")) : 0;
+static bool g_no_ll_defer = getenv("CD_NO_LL_DEFER") != nullptr;  // k_symm_ll: last-arrival fixup only
 
 // (the cooperative panel kernels launched with PDL as well measured no faster: N = 16384 reverse
 // 91.95 vs 91.94 ms, forward 95.46 vs 95.45 ms)
@@ -1036,6 +1039,29 @@ static int64_t g_fs_pieces = getenv("CD_FS_PIECES") ? atoi(getenv("CD_FS_PIECES"
 // 4.56 vs 4.66 ms with 32)
 static int64_t fs_pieces(int n) { return g_fs_pieces >= 0 ? g_fs_pieces : (n > 4096 ? 32 : 16); }
 static bool g_no_bal1 = getenv("CD_NO_BAL1") != nullptr;  // forward panel: one CTA per 128-wide K chunk
+// k_fwd_sk with a deferred fixup (k_fwd_sk_reduce) whenever >= 4 k-tiles per CTA would leave SMs
+// idle: one k-tile per CTA on up to every SM, the split tiles summed by the whole grid
+static bool g_no_fs_defer = getenv("CD_NO_FS_DEFER") != nullptr;
+// k_fwd_sk (fp.G / fp.defer chosen here); the caller has filled the rest of fp and called c.pre
+static void launch_fwd_sk(Ctx& c, FSParams& fp, const FSMaps& tm, int n, int64_t batch) {
+  fp.defer = !g_no_fs_defer && fp.total / LL_KT_PER_BLK < int64_t(c.sms) ? 1 : 0;
+  if (fp.defer) {
+    fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total)));
+  } else {
+    fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
+    // (fused sweep N = 4096: 12.54 -> 12.12 ms with the piece cap)
+    if (fs_pieces(n) > 0) fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, fs_pieces(n) * batch * fp.m)));
+  }
+  c.err = note_cuda(launch_pdl(k_fwd_sk, fp.G, LL_THREADS, FS_SMEM, c.st, fp, tm));
+  c.launched();
+  if (fp.defer && c.ok()) {
+    c.pre(CD_PROF_REDUCE, 0.0);
+    const int64_t elems = (fp.total / fp.KT) * int64_t(LL_BM) * fp.w;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(c.sms) * 8, (elems + 255) / 256)));
+    c.err = note_cuda(launch_pdl(k_fwd_sk_reduce, grid, 256, 0, c.st, fp));
+    c.launched();
+  }
+}
 // reverse panel phase 1: 128-row tiles cut into up to this many sub-tiles when the panel has few
 // tiles (1 = whole tiles, and the 32 x 32-tile path for the fewest).  Measured with 4 against 1:
 // N = 16384 93.24 -> 92.36 ms, 8192 16.27 -> 15.43 ms, 4096 4.08 -> 3.73 ms, 1024 487 -> 466 us
@@ -1130,8 +1156,11 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       // CTAs: at most ~PIECES pieces per output tile -- the last-arriving CTA sums all pieces
       // of a tile alone, so with few tiles more CTAs cost more in the fixup than they save
       const int64_t pieces = g_ll_pieces;
-      lp.G = int(std::max<int64_t>(1, std::min<int64_t>({int64_t(c.sms), lp.total / LL_KT_PER_BLK,
-                                                         pieces * batch * int64_t(lp.m)})));
+      // (deferred fixup as for k_fwd_sk: ~one k-tile per CTA on every SM, k_symm_ll_reduce sums)
+      lp.defer = !g_no_ll_defer && lp.total / LL_KT_PER_BLK < int64_t(c.sms) ? 1 : 0;
+      lp.G = lp.defer ? int(std::min<int64_t>(c.sms, lp.total))
+                      : int(std::max<int64_t>(1, std::min<int64_t>({int64_t(c.sms), lp.total / LL_KT_PER_BLK,
+                                                                    pieces * batch * int64_t(lp.m)})));
       lp.part = llpart;
       lp.cnt = cnt;
       c.pre(CD_PROF_SYMM, 2.0 * double(p) * p * w * double(batch));
@@ -1141,6 +1170,13 @@ static void blocked_rev_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
       }
       c.err = note_cuda(launch_pdl(k_symm_ll, lp.G, LL_THREADS, LL_SMEM, c.st, lp, w < nb ? tm_short : tm));
       c.launched();
+      if (lp.defer && c.ok()) {
+        c.pre(CD_PROF_REDUCE, 0.0);
+        const int64_t elems = (lp.total / (LL_KT_PER_BLK * int64_t(lp.m))) * int64_t(LL_BM) * w;
+        const int rg = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(c.sms) * 8, (elems + 255) / 256)));
+        c.err = note_cuda(launch_pdl(k_symm_ll_reduce, rg, 256, 0, c.st, lp));
+        c.launched();
+      }
     }
     // Cbar <- Cbar D^{-1};  Dbar <- Dbar - tril(Cbar^T C);  Dbar <- chol_unblocked_rev(D, Dbar)
     // (Eq. 10) + S -- one cooperative kernel
@@ -1421,14 +1457,11 @@ static void blocked_fwd_ll(Ctx& c, int n, int nb, int64_t batch, Opnd L, Opnd A,
         c.err = CD_ERR_UNSUPPORTED;
         return;
       }
-      fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
-      if (fs_pieces(n) > 0) fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, fs_pieces(n) * batch * fp.m)));
       fp.part = skpart;
       fp.cnt = cnt;
       fp.chol = 0;
       c.pre(CD_PROF_SYMM, 2.0 * double(p) * w * (2.0 * q + w) * double(batch));
-      c.err = note_cuda(launch_pdl(k_fwd_sk, fp.G, LL_THREADS, FS_SMEM, c.st, fp, tm));
-      c.launched();
+      launch_fwd_sk(c, fp, tm, n, batch);
     }
     j_prev = j, k_prev = k, p_prev = p;
   }
@@ -1506,15 +1539,11 @@ static void chol_fwd_fused(Ctx& c, int n, int nb, int64_t batch, Opnd A, Opnd Ad
       c.err = CD_ERR_UNSUPPORTED;
       return;
     }
-    fp.G = int(std::max<int64_t>(1, std::min<int64_t>(c.sms, fp.total / LL_KT_PER_BLK)));
-    if (fs_pieces(n) > 0)  // (fused sweep N = 4096: 12.54 -> 12.12 ms)
-      fp.G = int(std::max<int64_t>(1, std::min<int64_t>(fp.G, fs_pieces(n) * batch * fp.m)));
     fp.part = skpart;
     fp.cnt = cnt;
     fp.chol = chol;
     c.pre(CD_PROF_SYMM, 2.0 * double(p) * w * double(chol ? q : 2.0 * q + w) * double(batch));
-    c.err = note_cuda(launch_pdl(k_fwd_sk, fp.G, LL_THREADS, FS_SMEM, c.st, fp, tm));
-    c.launched();
+    launch_fwd_sk(c, fp, tm, n, batch);
   };
   auto base_params = [&](PanelFwdParams& pf) {
     memset(&pf, 0, sizeof(pf));

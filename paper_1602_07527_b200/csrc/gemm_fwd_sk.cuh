@@ -48,6 +48,7 @@ struct FSParams {
   int* cnt;          // [batch * m], zero on entry, reset by the last CTA
   int chol;          // factorisation mode (chol_blocked): W = C - B R^T, one
                      // segment with A and B both from the `l` map (KT = q / 16)
+  int defer;         // split tiles: pieces only; k_fwd_sk_reduce (next launch) sums them
 };
 
 __global__ void __launch_bounds__(LL_THREADS, 1) k_fwd_sk(const FSParams p, const __grid_constant__ FSMaps tm) {
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(LL_THREADS, 1) k_fwd_sk(const FSParams p, cons
             __stcg(mine + r + c * LL_BM, acc[ii][jj][e]);
           }
     }
+    if (p.defer) continue;  // the pieces are summed by k_fwd_sk_reduce
     __threadfence();
     asm volatile("bar.sync 1, %0;\n" ::"n"(LL_CONSUMERS * 32) : "memory");
     const int c_lo = ll_cta_of(ts, p.total, p.G), c_hi = ll_cta_of(te - 1, p.total, p.G);
@@ -238,6 +240,12 @@ __global__ void __launch_bounds__(LL_THREADS, 1) k_fwd_sk(const FSParams p, cons
       if (tid == 0) p.cnt[tg] = 0;
     }
   }
+}
+
+// The deferred fixup of k_fwd_sk (p.defer): ll_sk_reduce (symm_ll.cuh) over its tiles.
+__global__ void __launch_bounds__(256) k_fwd_sk_reduce(const FSParams p) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: k_fwd_sk's pieces are complete
+  ll_sk_reduce(p.A, p.n, p.k, p.j, p.w, p.m, p.KT, p.G, p.total, p.part);
 }
 
 }  // namespace cd

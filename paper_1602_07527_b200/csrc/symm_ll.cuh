@@ -79,6 +79,7 @@ struct LLParams {
   int64_t total;   // batch * m * (128/BK)m k-tiles (< 2^31, checked by the host)
   double* part;    // [G][2][128*128] partial slots
   int* cnt;        // [batch * m] arrival counters (zero on entry, reset by the last CTA)
+  int defer;       // split tiles: pieces only; k_symm_ll_reduce (next launch) sums them
 };
 
 __device__ __forceinline__ int64_t ll_start(int64_t c, int64_t total, int G) { return (c * total) / G; }
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(LL_THREADS, 1) k_symm_ll(const LLParams p, con
             __stcg(mine + r + c * LL_BM, acc[ii][jj][e]);
           }
     }
+    if (p.defer) continue;  // the pieces are summed by k_symm_ll_reduce
     __threadfence();
     asm volatile("bar.sync 1, %0;\n" ::"n"(LL_CONSUMERS * 32) : "memory");
     const int c_lo = ll_cta_of(ts, p.total, p.G), c_hi = ll_cta_of(te - 1, p.total, p.G);
@@ -295,6 +297,39 @@ __global__ void __launch_bounds__(LL_THREADS, 1) k_symm_ll(const LLParams p, con
     }
     // s_flag is rewritten only after the next piece's first barrier
   }
+}
+
+// The deferred stream-K fixup (p.defer of k_symm_ll / k_fwd_sk): for every output tile split across
+// CTAs, D = Cin + the pieces in CTA order -- the sum the last-arriving CTA forms otherwise -- spread
+// over the whole grid, one element per thread, instead of one CTA reading every piece of its tile.
+// With few output tiles (mid N) the stream-K kernel then runs ~one k-tile per CTA on every SM
+// instead of >= 4 k-tiles on a few of them.  Tiles covered by one CTA were written by it: skipped.
+// Tiles: batch x m of 128 rows (from row k) x w columns (from column j), KT k-tiles each.
+__device__ __forceinline__ void ll_sk_reduce(const Opnd& A, int n, int k, int j, int w, int m, int KT, int G,
+                                             int64_t total, const double* __restrict__ part) {
+  const int64_t per = int64_t(LL_BM) * w;  // elements per output tile
+  const int64_t tot = (total / KT) * per;  // batch * m tiles
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int tg = int(e / per);
+    const int rc = int(e - int64_t(tg) * per), c = rc / LL_BM, r = rc - c * LL_BM;
+    const int ts = tg * KT, te = ts + KT;
+    const int c_lo = ll_cta_of(ts, total, G), c_hi = ll_cta_of(te - 1, total, G);
+    const int b = tg / m, i = tg - b * m;
+    const int r0 = k + LL_BM * i;
+    if (c_lo == c_hi || r0 + r >= n) continue;
+    double* Dp = optr_w<double>(A, b) + (r0 + r) + int64_t(j + c) * A.ld;
+    double acc = __ldcg(Dp);
+    for (int cc = c_lo; cc <= c_hi; ++cc) {
+      const int slot = 2 * cc + (ll_start(cc, total, G) >= ts ? 0 : 1);
+      acc += __ldcg(part + int64_t(slot) * LL_TILE + r + c * LL_BM);
+    }
+    __stcg(Dp, acc);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_symm_ll_reduce(const LLParams p) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: k_symm_ll's pieces are complete
+  ll_sk_reduce(p.A, p.n, p.k, p.j, p.w, p.m, LL_KT_PER_BLK * p.m, p.G, p.total, p.part);
 }
 
 }  // namespace cd
