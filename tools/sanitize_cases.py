@@ -29,8 +29,13 @@ def main():
         S = np.einsum("...ij,...kj->...ik", L, L)
         cd.chol_fwd_fused(dev(S), dev(np.tril(Sd)))
     # panel phase 1 on 64-row sub-tiles (7 tiles per panel at most) and the batched N = 32 kernel
-    L, Lb, _ = synthetic.draw(1024, 1)
+    L, Lb, Sd = synthetic.draw(1024, 1, sdot=True)
     cd.chol_rev(dev(L), dev(Lb))
+    cd.chol_fwd(dev(L), dev(np.tril(Sd)))  # k_fwd_sk with the deferred stream-K fixup (few output tiles)
+    if os.environ.get("CD_SAN_BIG", "1") != "0":  # k_symm_ll: in-kernel and deferred fixups, short first block
+        L, Lb, Sd = synthetic.draw(2048 + 40, 2, sdot=True)
+        cd.chol_rev(dev(L), dev(Lb))
+        cd.chol_fwd(dev(L), dev(np.tril(Sd)))
     L, Lb, _ = synthetic.draw_batch(32, 1000, seed=1)
     cd.chol_rev(dev(L), dev(Lb))
     torch.cuda.synchronize()
