@@ -1,5 +1,7 @@
 """Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck /
-synccheck) runs (measurement / QA tool, not the product path)."""
+synccheck) runs (measurement / QA tool, not the product path).  Round 2: compute-sanitizer is
+refused on this GPU pool (the runner exits 86 before starting it), so these cases were last run
+under it in round 1; the round-2 kernels are covered by the NaN-guarded parity tests instead."""
 import os
 import sys
 
