@@ -330,7 +330,8 @@ def bench_single_rev(args, dist: Dist):
             "bound": "tensor", "achieved": round(achieved, 2), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
             "peak_source": "measured fp64 DMMA issue rate on this pool (tools/microbench_fp64.cu -> "
-                           "profiles/r01_microbench_fp64.txt); MEASURED_PEAKS.json has no fp64 entry",
+                           "profiles/r01_microbench_fp64.txt; with its clock record, sustained 1965 MHz, in "
+                           "profiles/r02_microbench_fp64.txt); MEASURED_PEAKS.json has no fp64 entry",
             "frac_of_cublas_dgemm": round(achieved / CUBLAS_DGEMM_TFLOPS, 4),
             "traffic": load_traffic(dom),
             "per_launch_ms": round(per_launch_ms, 4), "launches": int(g_n),
