@@ -58,10 +58,19 @@ def test_config5_rev_n16384_whole_output():
     got = A.transpose(0, 1).cpu().numpy()  # column-major image
     del A, Ld
     torch.cuda.empty_cache()
+    # the host-buffer call that bench.py's "e2e" times (cd_chol_host, pinned column-major buffers)
+    pin_L = torch.from_numpy(Lc).pin_memory().transpose(0, 1)
+    pin_A = torch.from_numpy(Ac).pin_memory().transpose(0, 1)
+    cd.chol_host("rev", pin_L, pin_A, nb=nb)
+    got_host = pin_A.transpose(0, 1).numpy()
+    h2d, d2h = cd.host_bytes()
+    assert 0 < h2d < 0.7 * 2 * n * n * 8 and 0 < d2h < 0.7 * n * n * 8  # lower triangles only cross the bus
     assert oracle.chol_rev_colmajor_inplace(n, Lc, Ac) == 0  # the whole unblocked sweep, in place
     err = lower_err_img(got, Ac)
-    print(f"N={n} chol_rev whole-output error vs oracle: {err:.3e}")
+    err_host = lower_err_img(got_host, Ac)
+    print(f"N={n} chol_rev whole-output error vs oracle: {err:.3e} (device buffers), {err_host:.3e} (cd_chol_host)")
     assert err < TOL64
+    assert err_host < TOL64
 
 
 def test_config5_fwd_n16384_whole_output():
